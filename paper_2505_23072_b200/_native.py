@@ -1,0 +1,203 @@
+"""ctypes binding of libhbmload.so (the C ABI in include/hbmload.h).
+
+The library is built in-tree (``paper_2505_23072_b200/libhbmload.so``) by
+``__graft_entry__.build()`` / ``python -m paper_2505_23072_b200._build``.
+ctypes releases the GIL for the duration of every foreign call, so the
+I/O engine's blocking ``hl_execute_plan`` never stalls other Python threads
+(e.g. thread ranks of an in-process group).
+
+There is no fallback: if the library is missing, every entry point raises
+:class:`~paper_2505_23072_b200.errors.NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import NativeUnavailable, raise_native
+
+LIB_PATH = Path(__file__).resolve().parent / "libhbmload.so"
+
+HL_IO_AUTO, HL_IO_BUFFERED, HL_IO_DIRECT, HL_IO_CUFILE = 0, 1, 2, 3
+IO_MODE_NAMES = {HL_IO_BUFFERED: "buffered", HL_IO_DIRECT: "direct", HL_IO_CUFILE: "cufile"}
+IO_MODES = {"auto": HL_IO_AUTO, "buffered": HL_IO_BUFFERED, "direct": HL_IO_DIRECT, "cufile": HL_IO_CUFILE}
+
+
+class hl_config(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("workers", C.c_uint32),
+        ("chunk_bytes", C.c_uint64),
+        ("slots_per_worker", C.c_uint32),
+        ("io_mode", C.c_uint32),
+        ("numa_node", C.c_int32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+class hl_block(C.Structure):
+    _fields_ = [
+        ("file", C.c_uint32),
+        ("worker", C.c_uint32),
+        ("file_off", C.c_uint64),
+        ("len", C.c_uint64),
+        ("dev_dst", C.c_uint64),
+    ]
+
+
+class hl_plan_stats(C.Structure):
+    _fields_ = [
+        ("bytes", C.c_uint64),
+        ("seconds", C.c_double),
+        ("workers", C.c_uint32),
+        ("blocks", C.c_uint32),
+        ("direct_bytes", C.c_uint64),
+        ("buffered_bytes", C.c_uint64),
+        ("cufile_bytes", C.c_uint64),
+        ("ring_setup_seconds", C.c_double),
+        ("io_mode_used", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+class hl_desc(C.Structure):
+    _fields_ = [
+        ("src", C.c_uint64),
+        ("dst", C.c_uint64),
+        ("rows", C.c_uint64),
+        ("row_elems", C.c_uint64),
+        ("src_pitch", C.c_uint64),
+        ("src_dtype", C.c_uint32),
+        ("dst_dtype", C.c_uint32),
+    ]
+
+
+# name -> (restype, argtypes): every symbol include/hbmload.h declares
+SIGNATURES = {
+    "hl_version": (C.c_char_p, []),
+    "hl_last_error": (C.c_char_p, []),
+    "hl_abi_version": (C.c_int, []),
+    "hl_ctx_create": (C.c_int, [C.POINTER(hl_config), C.POINTER(C.c_void_p)]),
+    "hl_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "hl_ctx_config": (C.c_int, [C.c_void_p, C.POINTER(hl_config)]),
+    "hl_execute_plan": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32,
+                                  C.POINTER(hl_block), C.c_uint32, C.POINTER(hl_plan_stats)]),
+    "hl_transfer_from_file": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "hl_file_residency": (C.c_int, [C.c_char_p, C.POINTER(C.c_double)]),
+    "hl_drop_cache": (C.c_int, [C.c_char_p]),
+    "hl_gds_available": (C.c_int, []),
+    "hl_conversion_supported": (C.c_int, [C.c_uint32, C.c_uint32]),
+    "hl_gather": (C.c_int, [C.POINTER(hl_desc), C.c_uint32, C.c_void_p]),
+    "hl_gather_max_batch": (C.c_uint32, []),
+    "hl_kernel_launches": (C.c_uint64, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the CDLL with typed signatures."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise NativeUnavailable(
+                f"{p} is missing: build it with `python -m paper_2505_23072_b200._build` "
+                "(there is no CPU fallback for the load path)")
+        lib = C.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.hl_last_error().decode(errors="replace") if _lib is not None else ""
+        raise_native(rc, msg or f"native call failed with status {rc}")
+
+
+def conversion_supported(src_code: int, dst_code: int) -> bool:
+    return bool(load().hl_conversion_supported(src_code, dst_code))
+
+
+def kernel_launches() -> int:
+    return int(load().hl_kernel_launches())
+
+
+def gather(descs: list[tuple], stream_ptr: int) -> None:
+    """Enqueue ``[(src, dst, rows, row_elems, src_pitch, src_code, dst_code), ...]``."""
+    if not descs:
+        return
+    lib = load()
+    arr = (hl_desc * len(descs))(*[hl_desc(*d) for d in descs])
+    check(lib.hl_gather(arr, len(descs), C.c_void_p(stream_ptr)))
+
+
+class IoEngine:
+    """One hl_ctx: worker threads' pinned ring + streams for one device."""
+
+    def __init__(self, device: int, workers: int = 0, chunk_bytes: int = 0,
+                 slots_per_worker: int = 0, io_mode: str = "auto", numa_node: int = -1):
+        lib = load()
+        cfg = hl_config(device, workers, chunk_bytes, slots_per_worker, IO_MODES[io_mode], numa_node, 0)
+        h = C.c_void_p()
+        check(lib.hl_ctx_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._lib = lib
+        eff = hl_config()
+        check(lib.hl_ctx_config(h, C.byref(eff)))
+        self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_ if f != "reserved"}
+
+    def execute(self, paths: list[str], blocks: list[tuple[int, int, int, int, int]]) -> dict:
+        """blocks: (file_index, worker_hint, file_off, len, dev_dst). Blocking."""
+        lib = self._lib
+        cpaths = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
+        arr = (hl_block * len(blocks))(*[hl_block(*b) for b in blocks])
+        st = hl_plan_stats()
+        check(lib.hl_execute_plan(self._h, cpaths, len(paths), arr, len(blocks), C.byref(st)))
+        modes = [name for bit, name in IO_MODE_NAMES.items() if st.io_mode_used & (1 << bit)]
+        return {
+            "bytes": st.bytes, "seconds": st.seconds, "workers": st.workers, "blocks": st.blocks,
+            "direct_bytes": st.direct_bytes, "buffered_bytes": st.buffered_bytes,
+            "cufile_bytes": st.cufile_bytes, "ring_setup_seconds": st.ring_setup_seconds,
+            "io_modes": modes,
+        }
+
+    def transfer(self, path: str, file_off: int, length: int, dev_ptr: int) -> None:
+        check(self._lib.hl_transfer_from_file(self._h, os.fsencode(path), file_off, length,
+                                              C.c_void_p(dev_ptr)))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.hl_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def file_residency(path: str) -> float:
+    lib = load()
+    f = C.c_double()
+    check(lib.hl_file_residency(os.fsencode(path), C.byref(f)))
+    return f.value
+
+
+def drop_cache(path: str) -> None:
+    check(load().hl_drop_cache(os.fsencode(path)))
+
+
+def gds_available() -> bool:
+    return bool(load().hl_gds_available())

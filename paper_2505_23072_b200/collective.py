@@ -1,0 +1,439 @@
+"""Rank groups and the broadcast / scatter shuffle (ref pkg/src/aggload/collective.py).
+
+Two interchangeable group types serve the loader:
+
+* :class:`DistGroup` — the production path: one process per GPU over
+  ``torch.distributed`` (NCCL on NVLink 5 / NVSwitch). ``get_tensor`` is an
+  ``ncclBroadcast`` from the owner; ``get_sharded`` is one owner-side pack
+  kernel (all W shards, cast fused, in a single ``hl_gather`` launch) followed
+  by one grouped send/recv (``batch_isend_irecv``: ncclGroupStart/End, so
+  uneven remainder parts need no padding). Everything is
+  enqueued on the current stream: no host rendezvous per key. NCCL's ordering
+  contract replaces the reference's descriptor-checked rendezvous; with
+  ``check_order=True`` every collective first all-gathers its (op, key, src,
+  dim) descriptor and a disagreement raises ``RendezvousTimeout`` like the
+  reference (collective.py:149-159).
+* :class:`ProcessGroup` — the reference's in-process group (ranks are threads
+  sharing a Condition-variable rendezvous, generation counted, poisoned on
+  timeout), kept so reference-style multi-rank tests run unchanged on one
+  GPU. Its data moves are ``hl_gather`` kernels reading the owner's buffer.
+
+Partitioning (``partition``/``ShardSpec``) is the reference's arithmetic:
+equal parts, the first ``shape[dim] % W`` ranks get one more (ref 52-74).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import threading
+import time
+from dataclasses import dataclass
+
+import torch
+
+from . import kernels
+from .errors import BadDim, DimTooSmall, RendezvousTimeout, SpecMismatch
+from .format import DType, TensorMetadata
+
+__all__ = ["ProcessGroup", "SingleGroup", "DistGroup", "ShardSpec", "partition"]
+
+DEFAULT_TIMEOUT = 30.0
+
+
+@dataclass(frozen=True)
+class ShardSpec:
+    key: str
+    dim: int
+    world_size: int
+    full_shape: tuple[int, ...]
+    part_shapes: tuple[tuple[int, ...], ...]
+
+    def bounds(self, rank: int) -> tuple[int, int]:
+        lo = sum(p[self.dim] for p in self.part_shapes[:rank])
+        return lo, lo + self.part_shapes[rank][self.dim]
+
+    def to_json(self) -> dict:
+        return {"key": self.key, "dim": self.dim, "world_size": self.world_size,
+                "full_shape": list(self.full_shape), "part_shapes": [list(p) for p in self.part_shapes]}
+
+
+def partition(meta: TensorMetadata, dim: int, world_size: int) -> ShardSpec:
+    shape = tuple(meta.shape)
+    if dim < 0 or dim >= len(shape):
+        raise BadDim(f"dim {dim} out of range for shape {list(shape)}")
+    if shape[dim] < world_size:
+        raise DimTooSmall(f"cannot split dim {dim} of size {shape[dim]} across {world_size} ranks")
+    parts = []
+    for r in range(world_size):
+        lo, hi = kernels.shard_bounds(shape[dim], world_size, r)
+        p = list(shape)
+        p[dim] = hi - lo
+        parts.append(tuple(p))
+    return ShardSpec(meta.name, dim, world_size, shape, tuple(parts))
+
+
+# ------------------------------------------------------------------------ data moves
+def _fresh(pool, name: str, dtype: DType, shape: tuple[int, ...]):
+    from .tensorview import make_view
+
+    n = 1
+    for d in shape:
+        n *= d
+    nb = n * dtype.size_bytes
+    buf = pool.allocate(nb)
+    return buf, make_view(buf, 0, TensorMetadata(name, dtype, tuple(shape), (0, nb)))
+
+
+def clone_full(view, pool, name: str, dtype: DType | None = None):
+    """A fresh tensor in ``pool`` with ``view``'s bytes, optionally cast
+    (ref collective.py:313-315 and loader.py:490-499)."""
+    dtype = dtype or view.dtype
+    buf, out = _fresh(pool, name, dtype, view.shape)
+    src_ptr, keep = _source_ptr(view, pool.device)
+    kernels.run([kernels.copy_desc(src_ptr, buf.ptr, view.numel, view.dtype, dtype)], pool.device)
+    del keep  # stream-ordered: the caching allocator reuses it only for later work
+    return buf, out
+
+
+def clone_slice(view, dim: int, lo: int, hi: int, part_shape, pool, name: str, dtype: DType | None = None):
+    """A fresh contiguous copy of ``view[..., lo:hi, ...]`` along ``dim``
+    (ref collective.py:318-330), optionally cast in the same pass."""
+    dtype = dtype or view.dtype
+    buf, out = _fresh(pool, name, dtype, part_shape)
+    src_ptr, keep = _source_ptr(view, pool.device)
+    kernels.run([kernels.shard_desc(src_ptr, view.shape, dim, lo, hi, buf.ptr, view.dtype, dtype)], pool.device)
+    del keep
+    return buf, out
+
+
+def _source_ptr(view, device: torch.device) -> int:
+    """Device address of ``view`` readable from ``device``. Same device: the
+    view itself. Another GPU: a peer copy of the region first."""
+    if view.buffer.tensor.device == device:
+        return view.buffer.ptr + view.base_offset, None
+    region = view.buffer.tensor[view.base_offset : view.base_offset + view.nbytes]
+    tmp = torch.empty(view.nbytes + 16, dtype=torch.uint8, device=device)
+    tmp[: view.nbytes].copy_(region)
+    return tmp.data_ptr(), tmp
+
+
+# ------------------------------------------------------------------------ thread group
+@dataclass(frozen=True)
+class _Span:
+    """What crosses rank threads: a region descriptor, never the view object
+    (so the owner's live-view accounting is not held by peers; ref 265-283)."""
+
+    buffer: object
+    base_offset: int
+    dtype: DType
+    shape: tuple[int, ...]
+
+    @property
+    def numel(self) -> int:
+        n = 1
+        for d in self.shape:
+            n *= d
+        return n
+
+    @property
+    def nbytes(self) -> int:
+        return self.numel * self.dtype.size_bytes
+
+
+def _span_of(view) -> "_Span | None":
+    return None if view is None else _Span(view.buffer, view.base_offset, view.dtype, tuple(view.shape))
+
+
+class ProcessGroup:
+    """In-process ranks (threads) with rendezvous collectives (ref collective.py:77-256)."""
+
+    def __init__(self, world_size: int, timeout: float = DEFAULT_TIMEOUT):
+        if world_size < 1:
+            raise ValueError(f"world_size must be >= 1, got {world_size}")
+        self.world_size = world_size
+        self.timeout = timeout
+        self._cv = threading.Condition()
+        self._gen = 0
+        self._slots: dict[int, object] = {}
+        self._done: dict[int, list] = {}
+        self._poison: str | None = None
+
+    def rank_ids(self) -> range:
+        return range(self.world_size)
+
+    def _poison_now(self, reason: str) -> None:
+        self._poison = reason
+        self._cv.notify_all()
+
+    def exchange(self, rank: int, payload: object) -> dict[int, object]:
+        if not 0 <= rank < self.world_size:
+            raise ValueError(f"rank {rank} not in group of {self.world_size}")
+        if self.world_size == 1:
+            return {0: payload}
+        with self._cv:
+            if self._poison:
+                raise RendezvousTimeout(self._poison)
+            if rank in self._slots:
+                self._poison_now(f"rank {rank} issued a collective out of turn")
+                raise RendezvousTimeout(self._poison)
+            gen = self._gen
+            self._slots[rank] = payload
+            if len(self._slots) == self.world_size:
+                self._done[gen] = [dict(self._slots), self.world_size]
+                self._slots = {}
+                self._gen += 1
+                self._cv.notify_all()
+            else:
+                deadline = time.monotonic() + self.timeout
+                while gen not in self._done and not self._poison:
+                    left = deadline - time.monotonic()
+                    if left <= 0:
+                        self._poison_now(f"rank {rank} timed out after {self.timeout}s waiting for peers "
+                                         f"(collective #{gen}); a rank failed to arrive")
+                        break
+                    self._cv.wait(left)
+                if gen not in self._done:
+                    raise RendezvousTimeout(self._poison)
+            snap, left = self._done[gen]
+            if left == 1:
+                del self._done[gen]
+            else:
+                self._done[gen][1] = left - 1
+            return snap
+
+    def _checked_exchange(self, rank: int, desc: tuple, data: object) -> dict[int, object]:
+        entries = self.exchange(rank, (desc, data))
+        descs = {r: d for r, (d, _) in entries.items()}
+        if any(d != desc for d in descs.values()):
+            with self._cv:
+                self._poison_now(f"collective mismatch across ranks (ordering bug): rank {rank} issued "
+                                 f"{desc}, peers issued {sorted(set(descs.values()), key=repr)}")
+            raise RendezvousTimeout(self._poison)
+        return {r: x for r, (_, x) in entries.items()}
+
+    def abort(self, reason: str) -> None:
+        with self._cv:
+            self._poison_now(reason)
+
+    def agree(self, rank: int, src: int, value: object, tag: str = "") -> object:
+        if self.world_size == 1:
+            return value
+        return self._checked_exchange(rank, ("agree", tag, src), value if rank == src else None)[src]
+
+    def _finish(self, pool) -> None:
+        # receivers' kernels read the owner's buffer: complete them before the
+        # owner may consume (release) it
+        if pool is not None:
+            torch.cuda.current_stream(pool.device).synchronize()
+
+    def broadcast(self, rank: int, view, src: int, pool=None, tag: str = "", meta=None):
+        if not 0 <= src < self.world_size:
+            raise ValueError(f"src {src} not in group of {self.world_size}")
+        if self.world_size == 1:
+            if view is None:
+                raise SpecMismatch("broadcast source holds no view")
+            return view
+        if rank == src and view is not None:
+            torch.cuda.current_stream(view.buffer.tensor.device).synchronize()
+        payload = _span_of(view) if rank == src else None
+        span = self._checked_exchange(rank, ("broadcast", tag, src), payload)[src]
+        if span is None:
+            raise SpecMismatch(f"broadcast src rank {src} holds no view (tag={tag!r})")
+        if rank == src:
+            result = view
+        else:
+            if pool is None:
+                raise ValueError("non-source ranks need a destination pool")
+            _, result = clone_full(span, pool, tag or "broadcast")
+        self._finish(pool)
+        self._checked_exchange(rank, ("broadcast-done", tag, src), None)
+        return result
+
+    def scatter(self, rank: int, spec: ShardSpec, src: int, source_view=None, pool=None, tag: str = "",
+                dtype: DType | None = None, src_dtype: DType | None = None):
+        if spec.world_size != self.world_size:
+            raise SpecMismatch(f"spec is for world {spec.world_size}, group is {self.world_size}")
+        if self.world_size == 1:
+            if source_view is None:
+                raise SpecMismatch("scatter source holds no view")
+            return source_view
+        if rank == src and source_view is not None:
+            torch.cuda.current_stream(source_view.buffer.tensor.device).synchronize()
+        payload = _span_of(source_view) if rank == src else None
+        span = self._checked_exchange(rank, ("scatter", tag, src, spec.dim, spec.full_shape), payload)[src]
+        if span is None:
+            raise SpecMismatch(f"scatter src rank {src} holds no view (tag={tag!r})")
+        if span.shape != spec.full_shape:
+            raise SpecMismatch(f"source shape {list(span.shape)} does not match spec {list(spec.full_shape)}")
+        if pool is None:
+            raise ValueError("scatter needs a destination pool on every rank")
+        lo, hi = spec.bounds(rank)
+        _, result = clone_slice(span, spec.dim, lo, hi, spec.part_shapes[rank], pool,
+                                tag or spec.key, dtype)
+        self._finish(pool)
+        self._checked_exchange(rank, ("scatter-done", tag, src), None)
+        return result
+
+
+class SingleGroup(ProcessGroup):
+    """World of one (ref collective.py:258-262)."""
+
+    def __init__(self):
+        super().__init__(1)
+
+
+# ------------------------------------------------------------------------ torch.distributed
+class DistGroup:
+    """One process per GPU over ``torch.distributed`` (NCCL on GPUs, gloo on CPU).
+
+    ``rank`` arguments are group ranks, as in :class:`ProcessGroup`, so the
+    loader drives both group types through the same calls.
+    """
+
+    def __init__(self, group=None, device: torch.device | None = None, check_order: bool = False,
+                 timeout: float = DEFAULT_TIMEOUT):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed is not initialised")
+        self._dist = dist
+        self.pg = group
+        self.world_size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.timeout = timeout
+        self.check_order = check_order
+        self.backend = dist.get_backend(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if self.backend == "nccl" else torch.device("cpu")
+        self.device = torch.device(device)
+
+    def rank_ids(self) -> range:
+        return range(self.world_size)
+
+    def _global(self, r: int) -> int:
+        return r if self.pg is None else self._dist.get_global_rank(self.pg, r)
+
+    # -- control plane ---------------------------------------------------------------
+    def exchange(self, rank: int, payload: object) -> dict[int, object]:
+        out = [None] * self.world_size
+        self._dist.all_gather_object(out, payload, group=self.pg)
+        return dict(enumerate(out))
+
+    def check(self, desc: tuple) -> None:
+        """Optional ordering check (ref _checked_exchange): all ranks must issue
+        the same collective descriptor."""
+        if not self.check_order or self.world_size == 1:
+            return
+        digest = hashlib.sha1(repr(desc).encode()).hexdigest()
+        got = self.exchange(self.rank, (digest, desc))
+        if any(d != digest for d, _ in got.values()):
+            raise RendezvousTimeout(f"collective mismatch across ranks (ordering bug): rank {self.rank} issued "
+                                    f"{desc}, peers issued {sorted({repr(x) for _, x in got.values()})}")
+
+    def agree(self, rank: int, src: int, value: object, tag: str = "") -> object:
+        if self.world_size == 1:
+            return value
+        self.check(("agree", tag, src))
+        box = [value if rank == src else None]
+        self._dist.broadcast_object_list(box, src=self._global(src), group=self.pg,
+                                         device=self.device if self.backend == "nccl" else None)
+        return box[0]
+
+    def abort(self, reason: str) -> None:
+        raise RendezvousTimeout(reason)
+
+    # -- data plane (raw tensors; the loader wraps them into TensorViews) ----------------
+    def broadcast_tensor(self, t: torch.Tensor, src: int) -> None:
+        """In-place broadcast of a contiguous tensor from group rank ``src``."""
+        if self.world_size > 1 and t.numel():
+            self._dist.broadcast(t, src=self._global(src), group=self.pg)
+
+    def scatter_parts(self, rank: int, src: int, parts: list[torch.Tensor] | None, out: torch.Tensor) -> None:
+        """Owner ``src`` sends ``parts[r]`` to every other rank r (its own part
+        is already in ``out``); the others receive into ``out``. One grouped
+        send/recv (ncclGroupStart/End under torch), so uneven remainder parts
+        need no padding."""
+        dist = self._dist
+        if self.world_size == 1:
+            return
+        ops = []
+        if rank == src:
+            if parts is None or len(parts) != self.world_size:
+                raise SpecMismatch("scatter owner must provide one part per rank")
+            for r in range(self.world_size):
+                if r != src and parts[r].numel():
+                    ops.append(dist.P2POp(dist.isend, parts[r], self._global(r), group=self.pg))
+        elif out.numel():
+            ops.append(dist.P2POp(dist.irecv, out, self._global(src), group=self.pg))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    # -- TensorView level (what the loader calls; same signatures as ProcessGroup) -------------
+    def broadcast(self, rank: int, view, src: int, pool=None, tag: str = "", meta=None):
+        """ncclBroadcast from ``src``; receivers allocate from their own pool.
+        ``meta`` (every rank knows it from the headers) gives dtype and shape."""
+        if not 0 <= src < self.world_size:
+            raise ValueError(f"src {src} not in group of {self.world_size}")
+        self.check(("broadcast", tag, src))
+        if self.world_size == 1:
+            if view is None:
+                raise SpecMismatch("broadcast source holds no view")
+            return view
+        if rank == src:
+            if view is None:
+                raise SpecMismatch(f"broadcast src rank {src} holds no view (tag={tag!r})")
+            self.broadcast_tensor(view.buffer.tensor[view.base_offset : view.base_offset + view.nbytes], src)
+            return view
+        if pool is None or meta is None:
+            raise ValueError("non-source ranks need a destination pool and the tensor metadata")
+        buf, out = _fresh(pool, tag or meta.name, meta.dtype, tuple(meta.shape))
+        self.broadcast_tensor(buf.tensor[: out.nbytes], src)
+        return out
+
+    def scatter(self, rank: int, spec: ShardSpec, src: int, source_view=None, pool=None, tag: str = "",
+                dtype: DType | None = None, src_dtype: DType | None = None):
+        """Owner packs every rank's slice (cast fused) with ONE hl_gather launch
+        — its own slice straight into its result — then one grouped NCCL
+        send/recv delivers the rest. NVLink carries final-dtype bytes."""
+        if spec.world_size != self.world_size:
+            raise SpecMismatch(f"spec is for world {spec.world_size}, group is {self.world_size}")
+        self.check(("scatter", tag, src, spec.dim, spec.full_shape))
+        if self.world_size == 1:
+            if source_view is None:
+                raise SpecMismatch("scatter source holds no view")
+            return source_view
+        if pool is None:
+            raise ValueError("scatter needs a destination pool on every rank")
+        in_dtype = source_view.dtype if source_view is not None else src_dtype
+        if in_dtype is None:
+            raise ValueError("receivers must know the source dtype (src_dtype)")
+        out_dtype = dtype or in_dtype
+        esz = out_dtype.size_bytes
+        buf, out = _fresh(pool, tag or spec.key, out_dtype, spec.part_shapes[rank])
+        mine = buf.tensor[: out.nbytes]
+        if rank != src:
+            self.scatter_parts(rank, src, None, mine)
+            return out
+        if source_view is None:
+            raise SpecMismatch(f"scatter src rank {src} holds no view (tag={tag!r})")
+        if tuple(source_view.shape) != spec.full_shape:
+            raise SpecMismatch(f"source shape {list(source_view.shape)} does not match spec {list(spec.full_shape)}")
+        sizes = [math.prod(p) * esz for p in spec.part_shapes]
+        pack_bytes = sum(-(-sz // 16) * 16 for r, sz in enumerate(sizes) if r != src)
+        pack = torch.empty(pack_bytes + 16, dtype=torch.uint8, device=pool.device)
+        src_ptr = source_view.buffer.ptr + source_view.base_offset
+        parts, descs, cursor = [], [], 0
+        for r in range(self.world_size):
+            lo, hi = spec.bounds(r)
+            if r == src:
+                dst, part = buf.ptr, mine
+            else:
+                dst, part = pack.data_ptr() + cursor, pack[cursor : cursor + sizes[r]]
+                cursor += -(-sizes[r] // 16) * 16  # keep every part 16-byte aligned
+            descs.append(kernels.shard_desc(src_ptr, spec.full_shape, spec.dim, lo, hi, dst, in_dtype, out_dtype))
+            parts.append(part)
+        kernels.run(descs, pool.device)
+        self.scatter_parts(rank, src, parts, mine)
+        return out

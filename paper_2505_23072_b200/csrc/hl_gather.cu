@@ -1,0 +1,525 @@
+// hl_gather.cu — the batched gather / realign / shard / cast kernel (sm_100a).
+//
+// One launch processes a whole table of descriptors (include/hbmload.h,
+// hl_desc). Each descriptor is a strided 2-D copy with an optional dtype
+// conversion; together they express every byte-moving step of the loader:
+//   * realign   — a tensor that landed at a misaligned device offset (odd
+//                 header, GDS-style aligned landing) is copied to an aligned
+//                 slot (ref device.py:466-534 align_and_convert, in place there,
+//                 out of place here),
+//   * clone     — auto_release copy of a tensor out of its file buffer
+//                 (ref loader.py:490-499 _clone_of),
+//   * shard     — a rank's slice along dim d (ref collective.py:318-330
+//                 _clone_slice; rows = prod(shape[:d])),
+//   * cast      — BF16/F32 -> F16 and F16/BF16 -> F32, bit-exact with the
+//                 reference's numpy conversions (ref device.py:303-320).
+//
+// Work decomposition (no tensor cores: this is HBM-bound byte movement):
+//   * The table travels in the kernel parameter buffer (__grid_constant__,
+//     up to kMaxDescs entries, ~32 KB), i.e. it is device-resident constant
+//     data with no host->device copy and no allocation per launch.
+//   * The output of every descriptor is cut into warp units of 4 KiB (256
+//     16-byte output vectors). Units of all descriptors form one global range;
+//     each warp of a persistent grid (SM count x resident blocks) strides over
+//     it and finds its descriptor by a warp-uniform search of the prefix
+//     table ("warp-level descriptor dispatch").
+//   * Vector path: every lane produces whole 16-byte output vectors. The source
+//     span of a vector (8, 16 or 32 bytes depending on the conversion) may start
+//     at any byte; it is assembled from aligned 16-byte loads with a funnel
+//     shift, so every global access is a 16-byte aligned, coalesced
+//     transaction. Stores are 16-byte aligned streaming stores.
+//   * Element path: rows whose output length is not a multiple of 16 bytes
+//     (odd shard widths, tiny tensors, tails) fall back to per-element moves.
+//     Correct for every case the reference accepts; never hot for LLM shapes.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "hl_internal.h"
+
+namespace hl {
+
+enum Kind : uint8_t {
+  K_COPY1 = 0,  // identity, any dtype (raw bytes)
+  K_BF16_F16 = 1,
+  K_F32_F16 = 2,
+  K_F16_F32 = 3,
+  K_BF16_F32 = 4,
+};
+
+enum Mode : uint8_t { M_VEC = 0, M_ELEM = 1 };
+
+struct KDesc {
+  uint64_t src;        // byte address of element (0,0)
+  uint64_t dst;        // byte address of the contiguous output
+  uint64_t src_pitch;  // bytes between source rows
+  uint64_t unit_begin; // first global unit of this descriptor
+  uint64_t nvec;       // M_VEC: full 16 B output vectors; M_ELEM: total elements
+  uint64_t row_elems;  // M_ELEM: elements per row; M_VEC: vectors per row (0 = one row)
+  uint32_t tail;       // M_VEC single-row: trailing elements after the last full vector
+  uint8_t kind, mode, ss, ds;  // conversion kind, mode, src/dst element size
+};
+static_assert(sizeof(KDesc) == 56, "KDesc layout");
+
+constexpr int kMaxDescs = 560;  // 560*56 + 16 = 31376 B < 32764 B param limit
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kUnroll = 8;
+constexpr uint64_t kUnitVecs = 32 * kUnroll;   // 4 KiB of output per warp unit
+constexpr uint64_t kUnitElems = 32 * kUnroll;  // elements per unit on the element path
+
+struct Params {
+  uint32_t n;
+  uint32_t pad;
+  uint64_t total_units;
+  KDesc d[kMaxDescs];
+};
+
+// ---------------------------------------------------------------- conversions
+// numpy float32 -> float16 (npy_floatbits_to_halfbits): RNE, overflow -> inf,
+// NaN keeps sign and mant>>13 (forced non-zero), no quieting.
+__device__ __forceinline__ uint32_t np_f32_to_f16(uint32_t f) {
+  const uint32_t sgn = (f >> 16) & 0x8000u;
+  const uint32_t fexp = f & 0x7f800000u;
+  const uint32_t fsig = f & 0x007fffffu;
+  if (fexp >= 0x47800000u) {
+    if (fexp == 0x7f800000u && fsig) {
+      uint32_t r = 0x7c00u + (fsig >> 13);
+      r += (r == 0x7c00u);
+      return sgn + r;
+    }
+    return sgn + 0x7c00u;
+  }
+  if (fexp <= 0x38000000u) {
+    if (fexp < 0x33000000u) return sgn;
+    const uint32_t e = fexp >> 23;
+    uint32_t sig = (0x00800000u + fsig) >> (113 - e);
+    if (((sig & 0x3fffu) != 0x1000u) || (f & 0x7ffu)) sig += 0x1000u;
+    return sgn + (sig >> 13);
+  }
+  uint32_t sig = fsig;
+  if ((sig & 0x3fffu) != 0x1000u) sig += 0x1000u;
+  return sgn + ((sig >> 13) + ((fexp - 0x38000000u) >> 13));
+}
+
+// numpy float16 -> float32 (npy_halfbits_to_floatbits): exact, NaN payload kept.
+__device__ __forceinline__ uint32_t np_f16_to_f32(uint32_t h) {
+  const uint32_t sgn = (h & 0x8000u) << 16;
+  const uint32_t hexp = h & 0x7c00u;
+  const uint32_t hsig = h & 0x03ffu;
+  if (hexp == 0x7c00u) return sgn | 0x7f800000u | (hsig << 13);
+  if (hexp == 0) {
+    if (hsig == 0) return sgn;
+    // subnormal: normalise; value = hsig * 2^-24
+    const int lz = __clz(hsig) - 21;  // leading zeros within the 10-bit field (1..10)
+    const uint32_t m = (hsig << lz) & 0x3ffu;
+    const uint32_t e = 113u - (uint32_t)lz;  // f32 exponent of hsig * 2^-24
+    return sgn | (e << 23) | (m << 13);
+  }
+  return sgn | ((((h & 0x7fffu) + 0x1c000u)) << 13);
+}
+
+// Vectorised narrowing: two f32 bit patterns -> packed f16x2 (lo in bits 0..15).
+// The hardware RNE conversion equals numpy's for every non-NaN input (overflow
+// to inf, subnormal rounding); NaNs are patched to numpy's payload rule.
+__device__ __forceinline__ uint32_t f32x2_to_f16x2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(b)), "f"(__uint_as_float(a)));
+  if (((a & 0x7fffffffu) > 0x7f800000u) | ((b & 0x7fffffffu) > 0x7f800000u)) {
+    const uint32_t lo = np_f32_to_f16(a), hi = np_f32_to_f16(b);
+    r = lo | (hi << 16);
+  }
+  return r;
+}
+
+// Widening: f16 bits -> f32 bits, hardware exact path with NaN payload patch.
+__device__ __forceinline__ uint32_t f16_to_f32_bits(uint32_t h) {
+  if ((h & 0x7c00u) == 0x7c00u && (h & 0x3ffu)) return ((h & 0x8000u) << 16) | 0x7f800000u | ((h & 0x3ffu) << 13);
+  float f;
+  asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"((unsigned short)h));
+  return __float_as_uint(f);
+}
+
+// scalar conversion on raw element bits (element path)
+__device__ __forceinline__ uint64_t convert_scalar(uint64_t x, uint8_t kind) {
+  switch (kind) {
+    case K_BF16_F16: return np_f32_to_f16((uint32_t)x << 16);
+    case K_F32_F16: return np_f32_to_f16((uint32_t)x);
+    case K_F16_F32: return np_f16_to_f32((uint32_t)x & 0xffffu);
+    case K_BF16_F32: return (uint64_t)((uint32_t)x << 16);
+    default: return x;
+  }
+}
+
+// ---------------------------------------------------------------- memory ops
+__device__ __forceinline__ uint4 ldg16(const void* p) {
+  uint4 r;
+  asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint64_t ldg8(const void* p) {
+  uint64_t r;
+  asm("ld.global.nc.u64 %0, [%1];" : "=l"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg16(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// bytes [s, s+16) of the 32-byte concatenation a||b (s in 0..15), branch-free.
+__device__ __forceinline__ uint4 extract16(uint4 a, uint4 b, uint32_t s) {
+  uint32_t x0 = a.x, x1 = a.y, x2 = a.z, x3 = a.w, x4 = b.x, x5 = b.y, x6 = b.z, x7 = b.w;
+  const bool q2 = s & 8, q1 = s & 4;
+  // shift by two words
+  uint32_t y0 = q2 ? x2 : x0, y1 = q2 ? x3 : x1, y2 = q2 ? x4 : x2, y3 = q2 ? x5 : x3,
+           y4 = q2 ? x6 : x4, y5 = q2 ? x7 : x5;
+  // shift by one word
+  uint32_t z0 = q1 ? y1 : y0, z1 = q1 ? y2 : y1, z2 = q1 ? y3 : y2, z3 = q1 ? y4 : y3,
+           z4 = q1 ? y5 : y4;
+  const uint32_t r = (s & 3) * 8;
+  uint4 o;
+  o.x = __funnelshift_r(z0, z1, r);
+  o.y = __funnelshift_r(z1, z2, r);
+  o.z = __funnelshift_r(z2, z3, r);
+  o.w = __funnelshift_r(z3, z4, r);
+  return o;
+}
+
+// Source span of one output vector, NB bytes from an arbitrary address.
+template <int NB>
+struct Span {
+  uint4 v[NB >= 16 ? NB / 16 : 1];
+};
+
+template <int NB>
+__device__ __forceinline__ void load_span(const uint8_t* p, Span<NB>& out) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if constexpr (NB == 8) {
+    const uint32_t s = a & 7;
+    const uint64_t* b = reinterpret_cast<const uint64_t*>(a - s);
+    uint64_t lo = ldg8(b);
+    if (s) {
+      const uint64_t hi = ldg8(b + 1);
+      lo = (lo >> (8 * s)) | (hi << (64 - 8 * s));
+    }
+    out.v[0] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), 0, 0);
+  } else {
+    const uint32_t s = a & 15;
+    const uint4* b = reinterpret_cast<const uint4*>(a - s);
+    if (s == 0) {
+#pragma unroll
+      for (int i = 0; i < NB / 16; ++i) out.v[i] = ldg16(b + i);
+    } else {
+      uint4 c0 = ldg16(b);
+#pragma unroll
+      for (int i = 0; i < NB / 16; ++i) {
+        const uint4 c1 = ldg16(b + i + 1);
+        out.v[i] = extract16(c0, c1, s);
+        c0 = c1;
+      }
+    }
+  }
+}
+
+template <int K>
+struct KindTraits;
+template <> struct KindTraits<K_COPY1> { static constexpr int NB = 16; };
+template <> struct KindTraits<K_BF16_F16> { static constexpr int NB = 16; };
+template <> struct KindTraits<K_F32_F16> { static constexpr int NB = 32; };
+template <> struct KindTraits<K_F16_F32> { static constexpr int NB = 8; };
+template <> struct KindTraits<K_BF16_F32> { static constexpr int NB = 8; };
+
+template <int K>
+__device__ __forceinline__ uint4 convert_vec(const Span<KindTraits<K>::NB>& s) {
+  if constexpr (K == K_COPY1) {
+    return s.v[0];
+  } else if constexpr (K == K_BF16_F16) {
+    const uint4 v = s.v[0];
+    uint4 o;
+    o.x = f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
+    o.y = f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
+    o.z = f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
+    o.w = f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
+    return o;
+  } else if constexpr (K == K_F32_F16) {
+    uint4 o;
+    o.x = f32x2_to_f16x2(s.v[0].x, s.v[0].y);
+    o.y = f32x2_to_f16x2(s.v[0].z, s.v[0].w);
+    o.z = f32x2_to_f16x2(s.v[1].x, s.v[1].y);
+    o.w = f32x2_to_f16x2(s.v[1].z, s.v[1].w);
+    return o;
+  } else if constexpr (K == K_F16_F32) {
+    const uint32_t a = s.v[0].x, b = s.v[0].y;
+    return make_uint4(f16_to_f32_bits(a & 0xffffu), f16_to_f32_bits(a >> 16),
+                      f16_to_f32_bits(b & 0xffffu), f16_to_f32_bits(b >> 16));
+  } else {  // K_BF16_F32
+    const uint32_t a = s.v[0].x, b = s.v[0].y;
+    return make_uint4(a << 16, a & 0xffff0000u, b << 16, b & 0xffff0000u);
+  }
+}
+
+// ---------------------------------------------------------------- element path
+__device__ __forceinline__ uint64_t load_elem(const uint8_t* p, uint32_t sz) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & (sz - 1)) == 0) {
+    switch (sz) {
+      case 1: return *p;
+      case 2: return *reinterpret_cast<const uint16_t*>(p);
+      case 4: return *reinterpret_cast<const uint32_t*>(p);
+      default: return *reinterpret_cast<const uint64_t*>(p);
+    }
+  }
+  uint64_t x = 0;
+  for (uint32_t i = 0; i < sz; ++i) x |= (uint64_t)p[i] << (8 * i);
+  return x;
+}
+__device__ __forceinline__ void store_elem(uint8_t* p, uint32_t sz, uint64_t x) {
+  switch (sz) {  // dst is aligned to its element size (checked on the host)
+    case 1: *p = (uint8_t)x; break;
+    case 2: *reinterpret_cast<uint16_t*>(p) = (uint16_t)x; break;
+    case 4: *reinterpret_cast<uint32_t*>(p) = (uint32_t)x; break;
+    default: *reinterpret_cast<uint64_t*>(p) = x; break;
+  }
+}
+
+__device__ __forceinline__ void elem_move(const KDesc& d, uint64_t e) {
+  const uint64_t row = e / d.row_elems, col = e - row * d.row_elems;
+  const uint8_t* s = reinterpret_cast<const uint8_t*>(d.src) + row * d.src_pitch + col * d.ss;
+  uint8_t* o = reinterpret_cast<uint8_t*>(d.dst) + e * d.ds;
+  store_elem(o, d.ds, convert_scalar(load_elem(s, d.ss), d.kind));
+}
+
+// ---------------------------------------------------------------- vector unit
+template <int K>
+__device__ __forceinline__ void vec_unit(const KDesc& d, uint64_t lu, uint32_t lane) {
+  constexpr int NB = KindTraits<K>::NB;
+  constexpr int U = (NB == 32) ? kUnroll / 2 : kUnroll;  // keep live registers bounded
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(d.src);
+  uint8_t* dst = reinterpret_cast<uint8_t*>(d.dst);
+  const uint64_t vbeg = lu * kUnitVecs;
+  const uint64_t vend = min(vbeg + kUnitVecs, d.nvec);
+  const uint64_t vpr = d.row_elems;  // vectors per row; 0 = single contiguous row
+  for (uint64_t base = vbeg; base < vend; base += 32 * U) {
+    Span<NB> sp[U];
+    uint64_t vi[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint64_t v = base + k * 32 + lane;
+      vi[k] = v;
+      if (v < vend) {
+        uint64_t off;
+        if (vpr == 0) {
+          off = v * NB;
+        } else {
+          const uint64_t row = v / vpr;
+          off = row * d.src_pitch + (v - row * vpr) * NB;
+        }
+        load_span<NB>(src + off, sp[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (vi[k] < vend) stg16(dst + vi[k] * 16, convert_vec<K>(sp[k]));
+    }
+  }
+  // single-row tail (< 16 bytes of output) is done by the descriptor's last unit
+  if (d.tail && vend == d.nvec && (vbeg < vend || d.nvec == 0)) {
+    if (lane < d.tail) {
+      const uint64_t e = d.nvec * (16 / d.ds) + lane;
+      const uint8_t* s = src + e * d.ss;
+      store_elem(dst + e * d.ds, d.ds, convert_scalar(load_elem(s, d.ss), d.kind));
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t find_desc(const Params& p, uint64_t u, uint32_t hint) {
+  // descriptors are visited in increasing unit order by each warp: gallop from the hint
+  uint32_t lo = hint, hi = p.n;  // invariant: d[lo].unit_begin <= u
+  if (p.d[lo].unit_begin > u) lo = 0;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p.d[mid].unit_begin <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant__ Params p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  uint32_t di = 0;
+  for (uint64_t u = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); u < p.total_units; u += nwarps) {
+    di = find_desc(p, u, di);
+    const KDesc& d = p.d[di];
+    const uint64_t lu = u - d.unit_begin;
+    if (d.mode == M_ELEM) {
+      const uint64_t e0 = lu * kUnitElems;
+#pragma unroll 4
+      for (uint32_t k = 0; k < kUnroll; ++k) {
+        const uint64_t e = e0 + k * 32 + lane;
+        if (e < d.nvec) elem_move(d, e);
+      }
+    } else {
+      vec_unit<K>(d, lu, lane);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static const uint32_t kSize[13] = {1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8};
+
+static int conversion_kind(uint32_t s, uint32_t d) {
+  if (s > 12 || d > 12) return -1;
+  if (s == d) return K_COPY1;
+  if (s == HL_DT_BF16 && d == HL_DT_F16) return K_BF16_F16;
+  if (s == HL_DT_F32 && d == HL_DT_F16) return K_F32_F16;
+  if (s == HL_DT_F16 && d == HL_DT_F32) return K_F16_F32;
+  if (s == HL_DT_BF16 && d == HL_DT_F32) return K_BF16_F32;
+  return -1;
+}
+
+static std::atomic<uint64_t> g_launches{0};
+
+typedef void (*KernelFn)(Params);
+static KernelFn kernel_of(int kind) {
+  switch (kind) {
+    case K_COPY1: return gather_kernel<K_COPY1>;
+    case K_BF16_F16: return gather_kernel<K_BF16_F16>;
+    case K_F32_F16: return gather_kernel<K_F32_F16>;
+    case K_F16_F32: return gather_kernel<K_F16_F32>;
+    default: return gather_kernel<K_BF16_F32>;
+  }
+}
+
+struct DevInfo {
+  int sms = 0;
+  int blocks_per_sm[5] = {0, 0, 0, 0, 0};
+};
+
+static const DevInfo& dev_info() {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  DevInfo& di = cache[dev & 63];
+  if (di.sms == 0) {
+    cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+    for (int k = 0; k < 5; ++k) {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of(k), kThreads, 0);
+      di.blocks_per_sm[k] = b > 0 ? b : 1;
+    }
+  }
+  return di;
+}
+
+// Translate one ABI descriptor into the kernel form; returns units (0 = empty).
+static int make_kdesc(const hl_desc& h, uint32_t i, KDesc& k, uint64_t* units_out) {
+  *units_out = 0;
+  const int kind = conversion_kind(h.src_dtype, h.dst_dtype);
+  if (kind < 0) return set_error(HL_ECONV, "unsupported conversion %u -> %u (descriptor %u)", h.src_dtype, h.dst_dtype, i);
+  const uint32_t ss = kSize[h.src_dtype], ds = kSize[h.dst_dtype];
+  if (h.rows == 0 || h.row_elems == 0) return HL_OK;
+  if (!h.src || !h.dst) return set_error(HL_EINVAL, "descriptor %u: null pointer", i);
+  if (h.dst % ds) return set_error(HL_EALIGN, "descriptor %u: dst 0x%llx not aligned to %u", i, (unsigned long long)h.dst, ds);
+  k = KDesc{};
+  k.src = h.src;
+  k.dst = h.dst;
+  k.kind = (uint8_t)kind;
+  k.ss = (uint8_t)ss;
+  k.ds = (uint8_t)ds;
+  uint64_t rows = h.rows, relems = h.row_elems;
+  const uint64_t pitch = h.src_pitch;
+  if (rows > 1 && pitch == relems * ss) {  // contiguous rows collapse into one
+    relems *= rows;
+    rows = 1;
+  }
+  k.src_pitch = pitch;
+  const uint64_t out_row = relems * ds;
+  uint64_t units;
+  if (h.dst % 16 == 0 && (rows == 1 || out_row % 16 == 0)) {
+    k.mode = M_VEC;
+    if (rows == 1) {
+      k.nvec = out_row / 16;
+      k.tail = (uint32_t)((out_row % 16) / ds);
+      k.row_elems = 0;
+    } else {
+      k.nvec = rows * (out_row / 16);
+      k.row_elems = out_row / 16;
+    }
+    units = (k.nvec + kUnitVecs - 1) / kUnitVecs;
+    if (units == 0) units = 1;  // tail-only descriptor
+  } else {
+    k.mode = M_ELEM;
+    k.nvec = rows * relems;
+    k.row_elems = relems;
+    units = (k.nvec + kUnitElems - 1) / kUnitElems;
+  }
+  *units_out = units;
+  return HL_OK;
+}
+
+static int launch(int kind, Params& p, cudaStream_t stream) {
+  if (p.total_units == 0) return HL_OK;
+  const DevInfo& di = dev_info();
+  const uint64_t want = (p.total_units + kWarps - 1) / kWarps;
+  const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind];
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  kernel_of(kind)<<<grid, kThreads, 0, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HL_ECUDA, "gather launch failed: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  p.n = 0;
+  p.total_units = 0;
+  return HL_OK;
+}
+
+}  // namespace hl
+
+using namespace hl;
+
+extern "C" int hl_conversion_supported(uint32_t s, uint32_t d) { return conversion_kind(s, d) >= 0 ? 1 : 0; }
+
+extern "C" uint32_t hl_gather_max_batch(void) { return kMaxDescs; }
+
+extern "C" uint64_t hl_kernel_launches(void) { return g_launches.load(); }
+
+extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
+  clear_error();
+  if (n && !descs) return set_error(HL_EINVAL, "null descriptor table");
+  // validate everything before launching anything
+  for (uint32_t i = 0; i < n; ++i) {
+    KDesc k;
+    uint64_t units;
+    int rc = make_kdesc(descs[i], i, k, &units);
+    if (rc) return rc;
+  }
+  static thread_local Params* p = nullptr;  // ~31 KB: keep it off the stack
+  if (!p) p = new Params();
+  // one kernel specialisation per conversion kind present in the batch
+  for (int kind = 0; kind < 5; ++kind) {
+    p->n = 0;
+    p->total_units = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (conversion_kind(descs[i].src_dtype, descs[i].dst_dtype) != kind) continue;
+      KDesc k;
+      uint64_t units;
+      make_kdesc(descs[i], i, k, &units);
+      if (units == 0) continue;
+      k.unit_begin = p->total_units;
+      p->d[p->n++] = k;
+      p->total_units += units;
+      if (p->n == (uint32_t)kMaxDescs) {
+        int rc = launch(kind, *p, (cudaStream_t)stream);
+        if (rc) return rc;
+      }
+    }
+    int rc = launch(kind, *p, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return HL_OK;
+}

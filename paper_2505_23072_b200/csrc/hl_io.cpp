@@ -1,0 +1,542 @@
+// hl_io.cpp — bulk file -> HBM engine (the B200 replacement for the
+// reference's execute_plan / transfer_from_file, ref transfer.py:305-389 and
+// device.py:238-288).
+//
+// Data path per chunk (default chunk 16 MiB, 4 KiB aligned):
+//
+//   storage --pread (O_DIRECT, or buffered when the file is page-cache
+//   resident)--> pinned slot (worker-private ring, NUMA-local) --cudaMemcpyAsync
+//   on the worker's own stream--> HBM
+//
+// Every worker owns `slots_per_worker` pinned slots and one CUDA stream, so
+// reads of chunk i+1 overlap the DMA of chunk i and several copy streams keep
+// the PCIe link full. Chunks are claimed dynamically from one atomic cursor,
+// so one large file is read by all workers in parallel (the reference's rule
+// of one thread per file leaves a 2-file Llama-7B load with two readers,
+// ref transfer.py:197-201). With HL_IO_CUFILE the chunk goes storage -> HBM
+// directly through cuFileRead (GPUDirect Storage when nvidia-fs is loaded;
+// cuFile's own compat mode otherwise), loaded with dlopen so the library
+// has no hard dependency on libcufile.
+//
+// The ring is allocated once per context (lazily, inside the workers so the
+// pages are first-touched on the workers' NUMA node) and reused by every
+// later plan; its cost is reported in hl_plan_stats.ring_setup_seconds.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <sched.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "hl_internal.h"
+
+namespace hl {
+
+static constexpr uint64_t kAlign = 4096;
+static inline uint64_t round_down(uint64_t x, uint64_t a) { return x / a * a; }
+static inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------ cuFile (dlopen)
+// Minimal mirror of the cufile.h types we use; layouts follow cufile.h 1.14.
+struct CUfileError { int err; int cu_err; };
+struct CUfileDescr {
+  int type;  // CU_FILE_HANDLE_TYPE_OPAQUE_FD = 1
+  union { int fd; void* handle; } handle;
+  const void* fs_ops;
+};
+struct CuFileApi {
+  bool tried = false, ok = false;
+  CUfileError (*driver_open)(void) = nullptr;
+  CUfileError (*handle_register)(void**, CUfileDescr*) = nullptr;
+  void (*handle_deregister)(void*) = nullptr;
+  ssize_t (*read)(void*, void*, size_t, off_t, off_t) = nullptr;
+};
+static CuFileApi g_cufile;
+static std::mutex g_cufile_mu;
+
+static bool cufile_load(std::string* why) {
+  std::lock_guard<std::mutex> g(g_cufile_mu);
+  if (g_cufile.tried) {
+    if (!g_cufile.ok && why) *why = "libcufile unavailable or cuFileDriverOpen failed";
+    return g_cufile.ok;
+  }
+  g_cufile.tried = true;
+  void* h = dlopen("libcufile.so.0", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libcufile.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    if (why) *why = std::string("dlopen libcufile: ") + dlerror();
+    return false;
+  }
+  g_cufile.driver_open = (CUfileError(*)(void))dlsym(h, "cuFileDriverOpen");
+  g_cufile.handle_register = (CUfileError(*)(void**, CUfileDescr*))dlsym(h, "cuFileHandleRegister");
+  g_cufile.handle_deregister = (void (*)(void*))dlsym(h, "cuFileHandleDeregister");
+  g_cufile.read = (ssize_t(*)(void*, void*, size_t, off_t, off_t))dlsym(h, "cuFileRead");
+  if (!g_cufile.driver_open || !g_cufile.handle_register || !g_cufile.read) {
+    if (why) *why = "libcufile lacks the expected symbols";
+    return false;
+  }
+  CUfileError e = g_cufile.driver_open();
+  if (e.err != 0) {
+    if (why) *why = "cuFileDriverOpen failed (code " + std::to_string(e.err) + ")";
+    return false;
+  }
+  g_cufile.ok = true;
+  return true;
+}
+
+// ------------------------------------------------------------------ topology
+static int gpu_numa_node(int dev) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return -1;
+  for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
+  char path[128];
+  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
+  FILE* f = fopen(path, "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+
+static std::vector<int> node_cpus(int node) {
+  std::vector<int> cpus;
+  if (node < 0) return cpus;
+  char path[128];
+  snprintf(path, sizeof path, "/sys/devices/system/node/node%d/cpulist", node);
+  FILE* f = fopen(path, "r");
+  if (!f) return cpus;
+  char buf[4096];
+  if (fgets(buf, sizeof buf, f)) {
+    char* save = nullptr;
+    for (char* tok = strtok_r(buf, ",\n", &save); tok; tok = strtok_r(nullptr, ",\n", &save)) {
+      int a, b;
+      if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+        for (int c = a; c <= b; ++c) cpus.push_back(c);
+      } else if (sscanf(tok, "%d", &a) == 1) {
+        cpus.push_back(a);
+      }
+    }
+  }
+  fclose(f);
+  return cpus;
+}
+
+}  // namespace hl
+
+using namespace hl;
+
+struct Slot {
+  uint8_t* host = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool busy = false;
+};
+struct WorkerRing {
+  std::vector<Slot> slots;
+  cudaStream_t stream = nullptr;
+  size_t next = 0;
+};
+
+struct hl_ctx {
+  hl_config cfg{};
+  std::vector<int> cpus;
+  std::vector<WorkerRing> rings;
+  bool ring_ready = false;
+  uint64_t slot_bytes = 0;
+  std::mutex mu;  // one plan at a time per context
+};
+
+namespace {
+
+struct Chunk {
+  uint32_t file;
+  uint64_t off, len, dst;
+};
+
+struct FileState {
+  int bfd = -1, dfd = -1;  // buffered / O_DIRECT descriptors
+  int mode = HL_IO_BUFFERED;
+  void* cufh = nullptr;
+  uint64_t size = 0;
+};
+
+struct PlanRun {
+  hl_ctx* ctx;
+  const std::vector<Chunk>* chunks;
+  std::vector<FileState>* files;
+  std::atomic<size_t> cursor{0};
+  std::atomic<bool> failed{false};
+  std::mutex err_mu;
+  int err_code = HL_OK;
+  std::string err_msg;
+  std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0};
+  double ring_setup = 0;
+  std::mutex setup_mu;
+
+  void fail(int code, const std::string& msg) {
+    std::lock_guard<std::mutex> g(err_mu);
+    if (err_code == HL_OK) {
+      err_code = code;
+      err_msg = msg;
+    }
+    failed.store(true);
+  }
+};
+
+bool pread_full(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got, int* err) {
+  uint64_t done = 0;
+  while (done < len) {
+    ssize_t n = pread(fd, buf + done, len - done, (off_t)(off + done));
+    if (n < 0) {
+      if (errno == EINTR) continue;
+      *err = errno;
+      *got = done;
+      return false;
+    }
+    if (n == 0) break;  // EOF
+    done += (uint64_t)n;
+  }
+  *got = done;
+  *err = 0;
+  return true;
+}
+
+int ensure_ring(hl_ctx* ctx, WorkerRing& r) {
+  if (!r.slots.empty()) return HL_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return set_error(HL_ECUDA, "stream create: %s", cudaGetErrorString(e));
+  r.slots.resize(ctx->cfg.slots_per_worker);
+  for (auto& s : r.slots) {
+    e = cudaHostAlloc((void**)&s.host, ctx->slot_bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) return set_error(HL_ENOMEM, "pinned slot of %llu bytes: %s",
+                                           (unsigned long long)ctx->slot_bytes, cudaGetErrorString(e));
+    e = cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return set_error(HL_ECUDA, "event create: %s", cudaGetErrorString(e));
+  }
+  return HL_OK;
+}
+
+void worker_main(PlanRun* run, uint32_t w) {
+  hl_ctx* ctx = run->ctx;
+  cudaSetDevice(ctx->cfg.device);
+  if (!ctx->cpus.empty()) {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    for (int c : ctx->cpus) CPU_SET(c, &set);
+    sched_setaffinity(0, sizeof set, &set);
+  }
+  WorkerRing& ring = ctx->rings[w];
+  if (ring.slots.empty()) {
+    const double t0 = now_s();
+    int rc = ensure_ring(ctx, ring);
+    {
+      std::lock_guard<std::mutex> g(run->setup_mu);
+      run->ring_setup = std::max(run->ring_setup, now_s() - t0);
+    }
+    if (rc) {
+      run->fail(rc, hl_last_error());
+      return;
+    }
+  }
+  const auto& chunks = *run->chunks;
+  auto& files = *run->files;
+  while (!run->failed.load(std::memory_order_relaxed)) {
+    const size_t i = run->cursor.fetch_add(1);
+    if (i >= chunks.size()) break;
+    const Chunk& c = chunks[i];
+    FileState& f = files[c.file];
+    if (f.mode == HL_IO_CUFILE) {
+      ssize_t n = g_cufile.read(f.cufh, (void*)c.dst, c.len, (off_t)c.off, 0);
+      if (n < 0 || (uint64_t)n != c.len) {
+        run->fail(HL_EIO, "cuFileRead of " + std::to_string(c.len) + " bytes at " + std::to_string(c.off) +
+                              " returned " + std::to_string(n));
+        return;
+      }
+      run->cufile_bytes += c.len;
+      continue;
+    }
+    Slot& s = ring.slots[ring.next];
+    ring.next = (ring.next + 1) % ring.slots.size();
+    if (s.busy) {
+      cudaError_t e = cudaEventSynchronize(s.ev);
+      if (e != cudaSuccess) {
+        run->fail(HL_ECUDA, std::string("H2D completion: ") + cudaGetErrorString(e));
+        return;
+      }
+      s.busy = false;
+    }
+    uint64_t head = 0, got = 0;
+    int err = 0;
+    bool direct = (f.mode == HL_IO_DIRECT && f.dfd >= 0);
+    bool ok = false;
+    if (direct) {
+      const uint64_t aoff = round_down(c.off, kAlign);
+      head = c.off - aoff;
+      const uint64_t alen = round_up(head + c.len, kAlign);
+      ok = pread_full(f.dfd, s.host, alen, aoff, &got, &err);
+      if (!ok && err == EINVAL) {  // filesystem refused O_DIRECT after all: buffered
+        direct = false;
+      } else if (ok && got < head + c.len) {
+        run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(aoff + got));
+        return;
+      }
+    }
+    if (!direct) {
+      head = 0;
+      ok = pread_full(f.bfd, s.host, c.len, c.off, &got, &err);
+      if (ok && got < c.len) {
+        run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(c.off + got) + " (" +
+                              std::to_string(c.len - got) + " bytes short)");
+        return;
+      }
+    }
+    if (!ok) {
+      run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err));
+      return;
+    }
+    (direct ? run->direct_bytes : run->buffered_bytes) += c.len;
+    cudaError_t e = cudaMemcpyAsync((void*)c.dst, s.host + head, c.len, cudaMemcpyHostToDevice, ring.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(s.ev, ring.stream);
+    if (e != cudaSuccess) {
+      run->fail(HL_ECUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
+      return;
+    }
+    s.busy = true;
+  }
+  cudaError_t e = cudaStreamSynchronize(ring.stream);
+  for (auto& s : ring.slots) s.busy = false;
+  if (e != cudaSuccess) run->fail(HL_ECUDA, std::string("H2D stream: ") + cudaGetErrorString(e));
+}
+
+double residency(int fd, uint64_t size) {
+  if (size == 0) return 1.0;
+  void* m = mmap(nullptr, size, PROT_READ, MAP_SHARED, fd, 0);
+  if (m == MAP_FAILED) return 0.0;
+  const long pg = sysconf(_SC_PAGESIZE);
+  const size_t pages = (size + pg - 1) / pg;
+  std::vector<unsigned char> vec(pages);
+  double frac = 0.0;
+  if (mincore(m, size, vec.data()) == 0) {
+    size_t res = 0;
+    for (unsigned char v : vec) res += v & 1;
+    frac = (double)res / (double)pages;
+  }
+  munmap(m, size);
+  return frac;
+}
+
+}  // namespace
+
+extern "C" int hl_ctx_create(const hl_config* cfg, hl_ctx** out) {
+  clear_error();
+  if (!out) return set_error(HL_EINVAL, "null output pointer");
+  hl_ctx* ctx = new hl_ctx();
+  if (cfg) ctx->cfg = *cfg;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    delete ctx;
+    return set_error(HL_ECUDA, "no CUDA device visible: %s", cudaGetErrorString(e));
+  }
+  if (ctx->cfg.device < 0 || ctx->cfg.device >= ndev) {
+    int d = ctx->cfg.device;
+    delete ctx;
+    return set_error(HL_EINVAL, "device %d out of range (%d visible)", d, ndev);
+  }
+  if (ctx->cfg.io_mode > HL_IO_CUFILE) {
+    delete ctx;
+    return set_error(HL_EINVAL, "unknown io_mode %u", cfg->io_mode);
+  }
+  int node = ctx->cfg.numa_node;
+  if (node < 0) node = gpu_numa_node(ctx->cfg.device);
+  ctx->cfg.numa_node = node;
+  ctx->cpus = node_cpus(node);
+  if (ctx->cfg.workers == 0) {
+    long n = ctx->cpus.empty() ? sysconf(_SC_NPROCESSORS_ONLN) : (long)ctx->cpus.size();
+    long w = (long)(0.8 * (double)n);
+    ctx->cfg.workers = (uint32_t)std::max(1L, std::min(w, 16L));
+  }
+  if (ctx->cfg.chunk_bytes == 0) ctx->cfg.chunk_bytes = 16ull << 20;
+  ctx->cfg.chunk_bytes = round_up(ctx->cfg.chunk_bytes, kAlign);
+  if (ctx->cfg.slots_per_worker == 0) ctx->cfg.slots_per_worker = 3;
+  ctx->slot_bytes = ctx->cfg.chunk_bytes + 2 * kAlign;  // O_DIRECT head/tail slack
+  ctx->rings.resize(ctx->cfg.workers);
+  *out = ctx;
+  return HL_OK;
+}
+
+extern "C" int hl_ctx_config(const hl_ctx* ctx, hl_config* out) {
+  if (!ctx || !out) return set_error(HL_EINVAL, "null argument");
+  *out = ctx->cfg;
+  return HL_OK;
+}
+
+extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
+  clear_error();
+  if (!ctx) return HL_OK;
+  cudaSetDevice(ctx->cfg.device);
+  for (auto& r : ctx->rings) {
+    if (r.stream) cudaStreamSynchronize(r.stream);
+    for (auto& s : r.slots) {
+      if (s.ev) cudaEventDestroy(s.ev);
+      if (s.host) cudaFreeHost(s.host);
+    }
+    if (r.stream) cudaStreamDestroy(r.stream);
+  }
+  delete ctx;
+  return HL_OK;
+}
+
+extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n_files, const hl_block* blocks,
+                               uint32_t n_blocks, hl_plan_stats* stats) {
+  clear_error();
+  if (!ctx) return set_error(HL_EINVAL, "null context");
+  if (n_blocks && (!blocks || !paths)) return set_error(HL_EINVAL, "null blocks or paths");
+  std::lock_guard<std::mutex> guard(ctx->mu);
+  const double t0 = now_s();
+  cudaSetDevice(ctx->cfg.device);
+
+  // split blocks into chunks (block order preserved)
+  std::vector<Chunk> chunks;
+  std::vector<char> used(n_files, 0);
+  uint64_t total = 0;
+  for (uint32_t b = 0; b < n_blocks; ++b) {
+    const hl_block& bl = blocks[b];
+    if (bl.file >= n_files) return set_error(HL_EINVAL, "block %u names file %u of %u", b, bl.file, n_files);
+    if (bl.len && !bl.dev_dst) return set_error(HL_EINVAL, "block %u has a null destination", b);
+    used[bl.file] = 1;
+    for (uint64_t o = 0; o < bl.len; o += ctx->cfg.chunk_bytes) {
+      const uint64_t n = std::min<uint64_t>(ctx->cfg.chunk_bytes, bl.len - o);
+      chunks.push_back({bl.file, bl.file_off + o, n, bl.dev_dst + o});
+    }
+    total += bl.len;
+  }
+
+  // open files, pick the read mode per file
+  std::vector<FileState> files(n_files);
+  auto close_all = [&]() {
+    for (auto& f : files) {
+      if (f.cufh && g_cufile.handle_deregister) g_cufile.handle_deregister(f.cufh);
+      if (f.bfd >= 0) close(f.bfd);
+      if (f.dfd >= 0) close(f.dfd);
+    }
+  };
+  uint32_t mode_mask = 0;
+  for (uint32_t i = 0; i < n_files; ++i) {
+    if (!used[i]) continue;
+    FileState& f = files[i];
+    f.bfd = open(paths[i], O_RDONLY | O_CLOEXEC);
+    if (f.bfd < 0) {
+      int err = errno;
+      close_all();
+      return set_error(HL_EIO, "cannot open %s: %s", paths[i], strerror(err));
+    }
+    struct stat st;
+    fstat(f.bfd, &st);
+    f.size = (uint64_t)st.st_size;
+    uint32_t mode = ctx->cfg.io_mode;
+    if (mode == HL_IO_AUTO) mode = residency(f.bfd, f.size) >= 0.5 ? HL_IO_BUFFERED : HL_IO_DIRECT;
+    if (mode == HL_IO_DIRECT || mode == HL_IO_CUFILE) {
+      f.dfd = open(paths[i], O_RDONLY | O_DIRECT | O_CLOEXEC);
+      if (f.dfd < 0 && mode == HL_IO_DIRECT) mode = HL_IO_BUFFERED;  // e.g. tmpfs: EINVAL
+    }
+    if (mode == HL_IO_CUFILE) {
+      std::string why;
+      if (!cufile_load(&why)) {
+        close_all();
+        return set_error(HL_EIO, "cuFile path requested but unavailable: %s", why.c_str());
+      }
+      CUfileDescr d{};
+      d.type = 1;
+      d.handle.fd = f.dfd >= 0 ? f.dfd : f.bfd;
+      CUfileError e = g_cufile.handle_register(&f.cufh, &d);
+      if (e.err != 0) {
+        close_all();
+        return set_error(HL_EIO, "cuFileHandleRegister(%s) failed (code %d)", paths[i], e.err);
+      }
+    }
+    f.mode = (int)mode;
+    mode_mask |= 1u << mode;
+  }
+  for (const Chunk& c : chunks) {
+    if (c.off + c.len > files[c.file].size) {
+      close_all();
+      return set_error(HL_EIO, "range [%llu, %llu) past end of %s (%llu bytes)", (unsigned long long)c.off,
+                       (unsigned long long)(c.off + c.len), paths[c.file], (unsigned long long)files[c.file].size);
+    }
+  }
+
+  PlanRun run;
+  run.ctx = ctx;
+  run.chunks = &chunks;
+  run.files = &files;
+  const uint32_t nw = (uint32_t)std::min<size_t>(ctx->cfg.workers, std::max<size_t>(chunks.size(), 1));
+  std::vector<std::thread> threads;
+  threads.reserve(nw);
+  for (uint32_t w = 0; w < nw; ++w) threads.emplace_back(worker_main, &run, w);
+  for (auto& t : threads) t.join();
+  close_all();
+  if (stats) {
+    memset(stats, 0, sizeof *stats);
+    stats->bytes = run.err_code == HL_OK ? total : 0;
+    stats->seconds = now_s() - t0;
+    stats->workers = nw;
+    stats->blocks = n_blocks;
+    stats->direct_bytes = run.direct_bytes.load();
+    stats->buffered_bytes = run.buffered_bytes.load();
+    stats->cufile_bytes = run.cufile_bytes.load();
+    stats->ring_setup_seconds = run.ring_setup;
+    stats->io_mode_used = mode_mask;
+  }
+  if (run.err_code != HL_OK) return set_error(run.err_code, "%s", run.err_msg.c_str());
+  return HL_OK;
+}
+
+extern "C" int hl_transfer_from_file(hl_ctx* ctx, const char* path, uint64_t file_off, uint64_t len, void* dev_dst) {
+  hl_block b{0, 0, file_off, len, (uint64_t)(uintptr_t)dev_dst};
+  if (len == 0) return HL_OK;
+  return hl_execute_plan(ctx, &path, 1, &b, 1, nullptr);
+}
+
+extern "C" int hl_file_residency(const char* path, double* frac) {
+  clear_error();
+  if (!path || !frac) return set_error(HL_EINVAL, "null argument");
+  int fd = open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return set_error(HL_EIO, "cannot open %s: %s", path, strerror(errno));
+  struct stat st;
+  fstat(fd, &st);
+  *frac = residency(fd, (uint64_t)st.st_size);
+  close(fd);
+  return HL_OK;
+}
+
+extern "C" int hl_drop_cache(const char* path) {
+  clear_error();
+  if (!path) return set_error(HL_EINVAL, "null path");
+  int fd = open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return set_error(HL_EIO, "cannot open %s: %s", path, strerror(errno));
+  fdatasync(fd);
+  int rc = posix_fadvise(fd, 0, 0, POSIX_FADV_DONTNEED);
+  close(fd);
+  if (rc) return set_error(HL_EIO, "posix_fadvise(%s): %s", path, strerror(rc));
+  return HL_OK;
+}
+
+extern "C" int hl_gds_available(void) {
+  return access("/proc/driver/nvidia-fs/stats", R_OK) == 0 ? 1 : 0;
+}

@@ -1,0 +1,247 @@
+"""Device memory on a B200: backends, buffers and the accounting pool.
+
+Reference counterpart: pkg/src/aggload/device.py (numpy byte arrays standing in
+for device memory). Here a :class:`DeviceBuffer` is a ``torch.uint8`` CUDA
+allocation from the torch caching allocator (the paper's "return GPU memory to
+the PyTorch memory pool"); :class:`DevicePool` keeps the
+reference's observable counters (allocated / pooled / cumulative pooled bytes,
+a capacity cap for out-of-memory tests) on top of it. Released buffers go back
+to torch's cache, which is the real pool; the counters are bookkeeping.
+
+Backends decide where a file's bytes land in its buffer:
+
+* ``host`` (ref DeviceBackend.host): the pinned-ring engine lands the body at
+  buffer offset 0, so a tensor sits at ``data_offsets.begin`` and is aligned
+  whenever the writer aligned it — no realign pass for odd-sized headers.
+* ``simdirect`` (ref DeviceBackend.sim_direct): GDS-shaped landing — the
+  transfer starts at the 512-byte floor of the body offset, exactly as the
+  reference's direct backend, so odd headers leave tensors misaligned and the
+  realign kernel repacks them (ref device.py:466-548).
+* ``gds``: cuFile (GPUDirect Storage) reads straight into HBM, 4 KiB landing.
+
+The bulk copy itself is the native engine (``_native.IoEngine``); the byte
+moves after landing (realign, clone, shard pack, cast) are ``hl_gather``.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass
+from enum import Enum
+
+import torch
+
+from . import _native
+from .errors import (
+    DoubleRelease,
+    NativeUnavailable,
+    OutOfBoundsView,
+    OutOfMemory,
+    UnsupportedConversion,
+)
+from .format import DType
+
+__all__ = [
+    "BackendKind",
+    "DeviceBackend",
+    "DeviceBuffer",
+    "DevicePool",
+    "DIRECT_ALIGNMENT",
+    "DEFAULT_HOST_BOUNCE",
+    "DEFAULT_ALIGN_BOUNCE",
+    "cuda_device",
+    "conversion_supported",
+]
+
+DIRECT_ALIGNMENT = 512               # ref device.py:51 (simdirect landing granularity)
+GDS_ALIGNMENT = 4096                 # cuFile / O_DIRECT block granularity
+DEFAULT_HOST_BOUNCE = 16 * 1024 * 1024  # pinned chunk per pread + H2D hop (ref: 160 MiB host bounce)
+DEFAULT_ALIGN_BOUNCE = 16 * 1024 * 1024  # kept for API parity; the realign kernel needs no bounce
+
+
+class BackendKind(Enum):
+    HOST = "host"
+    SIM_DIRECT = "simdirect"
+    GDS = "gds"
+
+
+@dataclass(frozen=True)
+class DeviceBackend:
+    """Landing rule + default I/O mode (ref device.py:61-81)."""
+
+    kind: BackendKind
+    transfer_alignment: int
+    bounce_buffer_bytes: int
+    io_mode: str = "auto"
+
+    @classmethod
+    def host(cls, bounce_buffer_bytes: int = DEFAULT_HOST_BOUNCE) -> "DeviceBackend":
+        return cls(BackendKind.HOST, 1, bounce_buffer_bytes, "auto")
+
+    @classmethod
+    def sim_direct(cls, bounce_buffer_bytes: int = DEFAULT_ALIGN_BOUNCE) -> "DeviceBackend":
+        return cls(BackendKind.SIM_DIRECT, DIRECT_ALIGNMENT, bounce_buffer_bytes, "auto")
+
+    @classmethod
+    def gds(cls, bounce_buffer_bytes: int = DEFAULT_HOST_BOUNCE) -> "DeviceBackend":
+        return cls(BackendKind.GDS, GDS_ALIGNMENT, bounce_buffer_bytes, "cufile")
+
+    @classmethod
+    def of(cls, kind: "str | BackendKind | DeviceBackend") -> "DeviceBackend":
+        if isinstance(kind, DeviceBackend):
+            return kind
+        if isinstance(kind, str):
+            kind = BackendKind(kind.lower())
+        if kind is BackendKind.HOST:
+            return cls.host()
+        if kind is BackendKind.GDS:
+            return cls.gds()
+        return cls.sim_direct()
+
+
+def cuda_device(index: int | None = None) -> torch.device:
+    """The CUDA device for a rank; refuses to run without one (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible: the load path runs only on the GPU")
+    n = torch.cuda.device_count()
+    idx = torch.cuda.current_device() if index is None else index % n
+    return torch.device("cuda", idx)
+
+
+def conversion_supported(src: DType, dst: DType) -> bool:
+    return _native.conversion_supported(src.code, dst.code)
+
+
+def check_conversion(src: DType, dst: DType, name: str = "") -> None:
+    if not conversion_supported(src, dst):
+        what = f"tensor {name!r}: " if name else ""
+        raise UnsupportedConversion(f"{what}{src.value} -> {dst.value} is not supported")
+
+
+class DeviceBuffer:
+    """One contiguous HBM allocation: the unit of bulk transfer and release
+    (ref device.py:84-130). ``tensor`` is the uint8 CUDA tensor; views made by
+    tensorview.make_view alias it without copying."""
+
+    def __init__(self, pool: "DevicePool", tensor: torch.Tensor, capacity: int):
+        self.pool = pool
+        self._tensor = tensor
+        self.capacity = int(capacity)
+        self.device_id = pool.device_id
+        self.backend = pool.backend
+        self.refcount = 0
+        self.released = False
+        self._live_views: weakref.WeakSet = weakref.WeakSet()
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        if self.released:
+            raise DoubleRelease(f"buffer on device {self.device_id} was already released")
+        return self._tensor
+
+    # reference spelling: the raw byte array behind the buffer
+    array = tensor
+
+    @property
+    def ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+    def _check_range(self, off: int, length: int) -> None:
+        if off < 0 or length < 0 or off + length > self.capacity:
+            raise OutOfBoundsView(f"range [{off}, {off + length}) outside buffer capacity {self.capacity}")
+
+    def write_bytes(self, off: int, data) -> None:
+        raw = bytes(data) if not isinstance(data, (bytes, bytearray)) else data
+        self._check_range(off, len(raw))
+        if raw:
+            src = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+            self.tensor[off : off + len(raw)].copy_(src)
+
+    def read_bytes(self, off: int, length: int) -> bytes:
+        self._check_range(off, length)
+        if length == 0:
+            return b""
+        return self.tensor[off : off + length].cpu().numpy().tobytes()
+
+    def live_view_count(self) -> int:
+        return len(self._live_views)
+
+    def release(self, *, force: bool = False, to_pool: bool = True) -> None:
+        self.pool.release(self, force=force, to_pool=to_pool)
+
+    def __repr__(self) -> str:
+        state = "released" if self.released else f"refcount={self.refcount}"
+        return f"DeviceBuffer(cuda:{self.device_id}, capacity={self.capacity}, {state})"
+
+
+class DevicePool:
+    """Accounting layer over the torch caching allocator (ref device.py:133-214).
+
+    ``allocate`` never zero-fills unless asked (every byte the loader reads was
+    written by the transfer or the kernel); ``release`` drops the pool's
+    reference so torch can recycle the memory, and moves the bytes from
+    ``allocated_bytes`` to ``pooled_bytes``. Exact-size reuse of a pooled
+    block is accounted like the reference.
+    """
+
+    def __init__(self, backend: DeviceBackend | str = "host", device_id: int | None = None,
+                 capacity_cap: int | None = None):
+        self.backend = DeviceBackend.of(backend)
+        self.device = cuda_device(device_id)
+        self.device_id = self.device.index
+        self.capacity_cap = capacity_cap
+        self._lock = threading.Lock()
+        self._free: dict[int, int] = {}
+        self.allocated_bytes = 0
+        self.pooled_bytes = 0
+        self.cumulative_pooled_bytes = 0
+
+    def allocate(self, size: int, zero: bool = False) -> DeviceBuffer:
+        if size < 0:
+            raise ValueError(f"allocation size must be non-negative, got {size}")
+        with self._lock:
+            if self._free.get(size):
+                self._free[size] -= 1
+                self.pooled_bytes -= size
+            else:
+                if self.capacity_cap is not None:
+                    while self.allocated_bytes + self.pooled_bytes + size > self.capacity_cap and self.pooled_bytes > 0:
+                        self._evict_one()
+                    if self.allocated_bytes + size > self.capacity_cap:
+                        raise OutOfMemory(
+                            f"device {self.device_id}: {size} bytes requested, "
+                            f"{self.allocated_bytes} live of {self.capacity_cap} cap")
+            try:
+                # +16: 16-byte vector loads of a tensor's last bytes stay inside the allocation
+                t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)
+            except torch.OutOfMemoryError as e:
+                raise OutOfMemory(f"device {self.device_id}: cannot allocate {size} bytes: {e}") from None
+            if zero:
+                t.zero_()
+            self.allocated_bytes += size
+            return DeviceBuffer(self, t, size)
+
+    def _evict_one(self) -> None:
+        for cap in sorted(self._free):
+            if self._free[cap]:
+                self._free[cap] -= 1
+                self.pooled_bytes -= cap
+                return
+
+    def release(self, buf: DeviceBuffer, *, force: bool = False, to_pool: bool = True) -> None:
+        with self._lock:
+            if buf.released:
+                raise DoubleRelease(f"buffer on device {self.device_id} released twice")
+            if not force:
+                if buf.refcount != 0:
+                    raise ValueError(f"buffer still hosts {buf.refcount} unconsumed keys; only close may force it")
+                if buf.live_view_count() > 0:
+                    raise ValueError(f"buffer has {buf.live_view_count()} live views; only close may force it")
+            buf.released = True
+            self.allocated_bytes -= buf.capacity
+            if to_pool:
+                self._free[buf.capacity] = self._free.get(buf.capacity, 0) + 1
+                self.pooled_bytes += buf.capacity
+                self.cumulative_pooled_bytes += buf.capacity
+            buf._tensor = None  # torch's caching allocator takes it back once views die

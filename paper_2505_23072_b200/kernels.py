@@ -1,0 +1,77 @@
+"""Descriptor builders over ``hl_gather`` (the batched realign/shard/cast kernel).
+
+Every byte move after landing goes through here, enqueued on the caller's
+current CUDA stream with no host synchronisation:
+
+* :func:`copy_desc`  — whole tensor, optionally cast (clone / realign / convert),
+* :func:`shard_desc` — rank slice ``[lo, hi)`` along ``dim`` of a row-major
+  tensor, optionally cast (ref collective.py:318-330 ``_clone_slice``; the
+  reference's oracle is reference.py:56-66 ``load_shard_bytes``),
+* :func:`run`        — launch a batch (one launch per conversion kind present).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _native
+from .format import DType
+
+Desc = tuple  # (src, dst, rows, row_elems, src_pitch, src_code, dst_code)
+
+
+def copy_desc(src_ptr: int, dst_ptr: int, numel: int, src: DType, dst: DType | None = None) -> Desc:
+    dst = dst or src
+    return (src_ptr, dst_ptr, 1 if numel else 0, numel, numel * src.size_bytes, src.code, dst.code)
+
+
+def shard_bounds(extent: int, world: int, rank: int) -> tuple[int, int]:
+    """Remainder-to-lower-ranks split (ref collective.py:62-67)."""
+    base, extra = divmod(extent, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def shard_desc(src_ptr: int, shape: tuple[int, ...], dim: int, lo: int, hi: int, dst_ptr: int,
+               src: DType, dst: DType | None = None) -> Desc:
+    dst = dst or src
+    outer = math.prod(shape[:dim])
+    inner = math.prod(shape[dim + 1:])
+    ss = src.size_bytes
+    rows = outer if (hi > lo and inner) else 0
+    return (src_ptr + lo * inner * ss, dst_ptr, rows, (hi - lo) * inner, shape[dim] * inner * ss,
+            src.code, dst.code)
+
+
+def stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+# Optional launch timing (bench.py): when a list, every run() appends
+# (start_event, end_event, algorithmic_bytes) recorded on the launch stream.
+TIMING: list | None = None
+
+_SIZE = [1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8]
+
+
+def algorithmic_bytes(descs: list[Desc]) -> int:
+    """Bytes a batch must move: source elements read + destination written."""
+    return sum(d[2] * d[3] * (_SIZE[d[5]] + _SIZE[d[6]]) for d in descs)
+
+
+def run(descs: list[Desc], device: torch.device) -> None:
+    """Enqueue the batch on ``device``'s current stream."""
+    if not descs:
+        return
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream(device)
+        if TIMING is None:
+            _native.gather(descs, stream.cuda_stream)
+            return
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _native.gather(descs, stream.cuda_stream)
+        e1.record(stream)
+        TIMING.append((e0, e1, algorithmic_bytes(descs)))

@@ -1,0 +1,74 @@
+"""The bulk file -> HBM engine (hl_execute_plan) in every I/O mode."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2505_23072_b200 import _native  # noqa: E402
+from paper_2505_23072_b200.errors import IoError  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["buffered", "direct", "auto", "cufile"]
+
+
+@pytest.fixture(scope="module")
+def blob(tmp_path_factory):
+    rng = np.random.default_rng(11)
+    data = rng.integers(0, 256, size=(37 << 20) + 4093, dtype=np.uint8)
+    p = tmp_path_factory.mktemp("io") / "blob.bin"
+    p.write_bytes(data.tobytes())
+    return p, data
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_ranges_land_exactly(blob, mode):
+    path, data = blob
+    eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode=mode)
+    rng = np.random.default_rng(3)
+    ranges = [(0, data.size), (1, 4095), (4096, 8192), (13281, (5 << 20) + 7), (data.size - 9, 9)]
+    for _ in range(6):
+        off = int(rng.integers(0, data.size - 1))
+        ranges.append((off, int(rng.integers(1, min(6 << 20, data.size - off)))))
+    total = sum(n for _, n in ranges)
+    dst = torch.zeros(total + 64, dtype=torch.uint8, device="cuda")
+    blocks, cur = [], 0
+    for i, (off, n) in enumerate(ranges):
+        blocks.append((0, i, off, n, dst.data_ptr() + cur))
+        cur += n
+    st = eng.execute([str(path)], blocks)
+    assert st["bytes"] == total
+    got = dst.cpu().numpy()
+    cur = 0
+    for off, n in ranges:
+        assert np.array_equal(got[cur:cur + n], data[off:off + n]), (mode, off, n)
+        cur += n
+    assert st["io_modes"], st
+    eng.close()
+
+
+def test_read_past_eof_is_io_error(blob):
+    path, data = blob
+    eng = _native.IoEngine(0, workers=2, chunk_bytes=1 << 20, io_mode="buffered")
+    dst = torch.zeros(8192, dtype=torch.uint8, device="cuda")
+    with pytest.raises(IoError):
+        eng.execute([str(path)], [(0, 0, data.size - 10, 100, dst.data_ptr())])
+    with pytest.raises(IoError):
+        eng.execute(["/nonexistent/file"], [(0, 0, 0, 10, dst.data_ptr())])
+
+
+def test_residency_and_drop_cache(blob):
+    path, data = blob
+    _ = path.read_bytes()  # warm
+    assert _native.file_residency(str(path)) > 0.5
+    _native.drop_cache(str(path))
+    assert _native.file_residency(str(path)) < 0.5
+    # auto mode now reads with O_DIRECT and still lands the right bytes
+    eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode="auto")
+    dst = torch.zeros(data.size, dtype=torch.uint8, device="cuda")
+    st = eng.execute([str(path)], [(0, 0, 0, data.size, dst.data_ptr())])
+    assert "direct" in st["io_modes"] or "buffered" in st["io_modes"]
+    assert np.array_equal(dst.cpu().numpy(), data)

@@ -1,0 +1,157 @@
+"""hl_gather (the sm_100a realign/shard/cast kernel) against the CPU oracle.
+
+Bit-exact comparisons over the whole destination buffer (pre-filled with a
+sentinel, so stray writes are caught too). The oracle is oracle/oracle_c.c
+(numpy's conversion algorithm, pinned to the reference's outputs by
+tests/golden/conv.npz).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle  # noqa: E402
+from paper_2505_23072_b200 import _native, kernels  # noqa: E402
+from paper_2505_23072_b200.errors import MisalignedDirectTransfer, UnsupportedConversion  # noqa: E402
+from paper_2505_23072_b200.format import DType  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8]
+CASTS = [(10, 9), (11, 9), (9, 11), (10, 11)]  # BF16->F16, F32->F16, F16->F32, BF16->F32
+SENTINEL = 0xA5
+
+
+def run_both(src: np.ndarray, dst_size: int, descs: list[tuple]):
+    """descs: (src_off, dst_off, rows, row_elems, pitch, sdt, ddt) relative to
+    the two buffers. Returns (gpu_bytes, oracle_bytes)."""
+    dev = torch.device("cuda", 0)
+    s = torch.from_numpy(src).to(dev)
+    d = torch.full((dst_size + 64,), SENTINEL, dtype=torch.uint8, device=dev)
+    kd = [(s.data_ptr() + so, d.data_ptr() + do, r, re, p, sd, dd) for so, do, r, re, p, sd, dd in descs]
+    _native.gather(kd, torch.cuda.current_stream(dev).cuda_stream)
+    got = d.cpu().numpy()
+    lib = oracle.clib()
+    exp = np.full(dst_size + 64, SENTINEL, dtype=np.uint8)
+    sp, ep = src.ctypes.data, exp.ctypes.data
+    for so, do, r, re, p, sd, dd in descs:
+        if r and re:
+            assert lib.oracle_gather(sp + so, ep + do, r, re, p, sd, dd) == 0
+    return got, exp
+
+
+def assert_same(got, exp):
+    if not np.array_equal(got, exp):
+        bad = np.nonzero(got != exp)[0]
+        raise AssertionError(f"{bad.size} bytes differ; first at {bad[:8]}: got {got[bad[:8]]} exp {exp[bad[:8]]}")
+
+
+@pytest.mark.parametrize("pair", CASTS)
+@pytest.mark.parametrize("src_shift", [0, 1, 2, 3, 5, 8, 13])
+def test_exhaustive_16bit_and_sampled_f32_casts(golden_conv, pair, src_shift):
+    sdt, ddt = pair
+    if sdt == 11:
+        vals = golden_conv["f32_in"].astype("<u4")
+        ref = golden_conv["f32_f16"]
+    else:
+        vals = golden_conv["all16"].astype("<u2")
+        ref = {(10, 9): golden_conv["bf16_f16"], (9, 11): golden_conv["f16_f32"],
+               (10, 11): golden_conv["bf16_f32"]}[pair]
+    raw = vals.tobytes()
+    src = np.zeros(len(raw) + 64, dtype=np.uint8)
+    src[src_shift:src_shift + len(raw)] = np.frombuffer(raw, np.uint8)
+    n = vals.size
+    out_bytes = n * SIZES[ddt]
+    got, exp = run_both(src, out_bytes, [(src_shift, 0, 1, n, len(raw), sdt, ddt)])
+    assert_same(got, exp)
+    # and the oracle itself equals the reference's outputs
+    assert got[:out_bytes].tobytes() == ref.tobytes()
+
+
+def _random_desc(rng, cursor_src, cursor_dst, src_cap):
+    if rng.random() < 0.3:
+        sdt, ddt = CASTS[int(rng.integers(0, 4))]
+    else:
+        sdt = int(rng.integers(0, 13))
+        ddt = sdt
+    ss, ds = SIZES[sdt], SIZES[ddt]
+    rows = int(rng.choice([1, 1, 2, 3, 7, 16, 33]))
+    row_elems = int(rng.choice([1, 2, 3, 5, 8, 15, 16, 64, 100, 257, 1024]))
+    pad = int(rng.choice([0, 0, 1, 3, 8, 17]))  # strided (shard-like) rows when pad > 0
+    pitch = (row_elems + pad) * ss
+    src_off = cursor_src + int(rng.integers(0, 16))  # any byte: realign
+    align = 16 if rng.random() < 0.7 else ds
+    dst_off = -(-cursor_dst // align) * align
+    need = src_off + (rows - 1) * pitch + row_elems * ss
+    if need > src_cap:
+        return None
+    return (src_off, dst_off, rows, row_elems, pitch, sdt, ddt), need, dst_off + rows * row_elems * ds
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_batches(seed):
+    rng = np.random.default_rng(seed)
+    src_cap = 1 << 22
+    src = rng.integers(0, 256, size=src_cap, dtype=np.uint8)
+    descs, cs, cd = [], 0, 0
+    for _ in range(int(rng.integers(50, 700))):  # > 560 exercises multi-launch batches
+        r = _random_desc(rng, cs, cd, src_cap)
+        if r is None:
+            break
+        d, cs, cd = r
+        descs.append(d)
+    got, exp = run_both(src, cd, descs)
+    assert_same(got, exp)
+
+
+@pytest.mark.parametrize("sdt,ddt", [(10, 10), (10, 9), (11, 9), (9, 11), (1, 1)])
+@pytest.mark.parametrize("shift", [0, 1, 6])
+def test_large_contiguous(sdt, ddt, shift):
+    rng = np.random.default_rng(7)
+    n = (48 << 20) // SIZES[sdt] + 3  # ~48 MiB plus a ragged tail
+    src = rng.integers(0, 256, size=n * SIZES[sdt] + 64, dtype=np.uint8)
+    got, exp = run_both(src, n * SIZES[ddt], [(shift, 0, 1, n, n * SIZES[sdt], sdt, ddt)])
+    assert_same(got, exp)
+
+
+@pytest.mark.parametrize("dim", [0, 1, 2])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_descriptors_match_reference_slicing(dim, world):
+    rng = np.random.default_rng(dim * 10 + world)
+    shape = (24, 40, 12)
+    dt = DType.BF16
+    raw = rng.integers(0, 256, size=int(np.prod(shape)) * 2, dtype=np.uint8)
+    src = np.concatenate([np.zeros(3, np.uint8), raw, np.zeros(64, np.uint8)])
+    dev = torch.device("cuda", 0)
+    s = torch.from_numpy(src).to(dev)
+    for rank in range(world):
+        lo, hi = kernels.shard_bounds(shape[dim], world, rank)
+        exp_shape, exp = oracle.slice_bytes(raw.tobytes(), "BF16", shape, dim, world, rank)
+        out = torch.full((len(exp) + 32,), SENTINEL, dtype=torch.uint8, device=dev)
+        kernels.run([kernels.shard_desc(s.data_ptr() + 3, shape, dim, lo, hi, out.data_ptr(), dt)], dev)
+        got = out.cpu().numpy()
+        assert got[: len(exp)].tobytes() == exp
+        assert (got[len(exp):] == SENTINEL).all()
+
+
+def test_errors_are_typed():
+    dev = torch.device("cuda", 0)
+    t = torch.zeros(64, dtype=torch.uint8, device=dev)
+    p = t.data_ptr()
+    with pytest.raises(UnsupportedConversion):
+        _native.gather([(p, p + 32, 1, 2, 8, 12, 9)], 0)  # F64 -> F16
+    with pytest.raises(MisalignedDirectTransfer):
+        _native.gather([(p, p + 33, 1, 2, 8, 11, 11)], 0)  # F32 dst at odd address
+
+
+def test_launch_counter_moves():
+    dev = torch.device("cuda", 0)
+    t = torch.zeros(1024, dtype=torch.uint8, device=dev)
+    before = _native.kernel_launches()
+    kernels.run([kernels.copy_desc(t.data_ptr(), t.data_ptr() + 512, 100, DType.F32)], dev)
+    assert _native.kernel_launches() == before + 1
