@@ -23,6 +23,7 @@
 // later plan; its cost is reported in hl_plan_stats.ring_setup_seconds.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <stdlib.h>
 #include <errno.h>
 #include <fcntl.h>
 #include <sched.h>
@@ -451,6 +452,11 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     f.size = (uint64_t)st.st_size;
     uint32_t mode = ctx->cfg.io_mode;
     if (mode == HL_IO_AUTO) mode = residency(f.bfd, f.size) >= 0.5 ? HL_IO_BUFFERED : HL_IO_DIRECT;
+    // cuFile only where it is real GPUDirect Storage (nvidia-fs loaded); without
+    // it cuFile's compat mode is a slower POSIX bounce path than our own ring,
+    // so the GDS-shaped backend reads with O_DIRECT instead (HL_FORCE_CUFILE=1
+    // keeps cuFile for experiments).
+    if (mode == HL_IO_CUFILE && !hl_gds_available() && !getenv("HL_FORCE_CUFILE")) mode = HL_IO_DIRECT;
     if (mode == HL_IO_DIRECT || mode == HL_IO_CUFILE) {
       f.dfd = open(paths[i], O_RDONLY | O_DIRECT | O_CLOEXEC);
       if (f.dfd < 0 && mode == HL_IO_DIRECT) mode = HL_IO_BUFFERED;  // e.g. tmpfs: EINVAL
