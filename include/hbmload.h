@@ -70,7 +70,9 @@ enum hl_io_mode {
   HL_IO_AUTO = 0,      /* per file: buffered if mostly page-cache resident, else O_DIRECT */
   HL_IO_BUFFERED = 1,  /* pread through the page cache into the pinned ring            */
   HL_IO_DIRECT = 2,    /* O_DIRECT pread (4 KiB aligned) into the pinned ring            */
-  HL_IO_CUFILE = 3     /* cuFileRead straight into HBM (GPUDirect Storage, nvidia-fs)    */
+  HL_IO_CUFILE = 3,    /* cuFileRead straight into HBM (GPUDirect Storage, nvidia-fs)    */
+  HL_IO_MMAP = 4       /* page-cache pages pinned in place (mmap + cudaHostRegister) and
+                          DMA'd straight to HBM: no CPU copy                                */
 };
 
 const char* hl_version(void);
@@ -109,8 +111,9 @@ typedef struct hl_plan_stats {
   uint64_t direct_bytes;    /* bytes read with O_DIRECT                       */
   uint64_t buffered_bytes;  /* bytes read through the page cache              */
   uint64_t cufile_bytes;    /* bytes read by cuFile                           */
+  uint64_t mmap_bytes;      /* bytes DMA'd from pinned page-cache pages        */
   double ring_setup_seconds;/* pinned ring allocation charged to this call    */
-  uint32_t io_mode_used;    /* bitmask: 1<<HL_IO_BUFFERED | 1<<HL_IO_DIRECT | 1<<HL_IO_CUFILE */
+  uint32_t io_mode_used;    /* bitmask of 1<<hl_io_mode actually used         */
   uint32_t reserved;
 } hl_plan_stats;
 

@@ -21,9 +21,10 @@ from .errors import NativeUnavailable, raise_native
 
 LIB_PATH = Path(__file__).resolve().parent / "libhbmload.so"
 
-HL_IO_AUTO, HL_IO_BUFFERED, HL_IO_DIRECT, HL_IO_CUFILE = 0, 1, 2, 3
-IO_MODE_NAMES = {HL_IO_BUFFERED: "buffered", HL_IO_DIRECT: "direct", HL_IO_CUFILE: "cufile"}
-IO_MODES = {"auto": HL_IO_AUTO, "buffered": HL_IO_BUFFERED, "direct": HL_IO_DIRECT, "cufile": HL_IO_CUFILE}
+HL_IO_AUTO, HL_IO_BUFFERED, HL_IO_DIRECT, HL_IO_CUFILE, HL_IO_MMAP = 0, 1, 2, 3, 4
+IO_MODE_NAMES = {HL_IO_BUFFERED: "buffered", HL_IO_DIRECT: "direct", HL_IO_CUFILE: "cufile", HL_IO_MMAP: "mmap"}
+IO_MODES = {"auto": HL_IO_AUTO, "buffered": HL_IO_BUFFERED, "direct": HL_IO_DIRECT, "cufile": HL_IO_CUFILE,
+            "mmap": HL_IO_MMAP}
 
 
 class hl_config(C.Structure):
@@ -57,6 +58,7 @@ class hl_plan_stats(C.Structure):
         ("direct_bytes", C.c_uint64),
         ("buffered_bytes", C.c_uint64),
         ("cufile_bytes", C.c_uint64),
+        ("mmap_bytes", C.c_uint64),
         ("ring_setup_seconds", C.c_double),
         ("io_mode_used", C.c_uint32),
         ("reserved", C.c_uint32),
@@ -168,7 +170,8 @@ class IoEngine:
         return {
             "bytes": st.bytes, "seconds": st.seconds, "workers": st.workers, "blocks": st.blocks,
             "direct_bytes": st.direct_bytes, "buffered_bytes": st.buffered_bytes,
-            "cufile_bytes": st.cufile_bytes, "ring_setup_seconds": st.ring_setup_seconds,
+            "cufile_bytes": st.cufile_bytes, "mmap_bytes": st.mmap_bytes,
+            "ring_setup_seconds": st.ring_setup_seconds,
             "io_modes": modes,
         }
 

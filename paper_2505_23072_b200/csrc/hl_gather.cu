@@ -70,12 +70,17 @@ constexpr int kUnroll = 8;
 constexpr uint64_t kUnitVecs = 32 * kUnroll;   // 4 KiB of output per warp unit
 constexpr uint64_t kUnitElems = 32 * kUnroll;  // elements per unit on the element path
 
-struct Params {
+constexpr int kSmallDescs = 4;  // single-key calls launch with a 240-byte parameter block
+
+template <int N>
+struct ParamsN {
   uint32_t n;
   uint32_t pad;
   uint64_t total_units;
-  KDesc d[kMaxDescs];
+  KDesc d[N];
 };
+using Params = ParamsN<kMaxDescs>;
+using SmallParams = ParamsN<kSmallDescs>;
 
 // ---------------------------------------------------------------- conversions
 // numpy float32 -> float16 (npy_floatbits_to_halfbits): RNE, overflow -> inf,
@@ -335,7 +340,8 @@ __device__ __forceinline__ void vec_unit(const KDesc& d, uint64_t lu, uint32_t l
   }
 }
 
-__device__ __forceinline__ uint32_t find_desc(const Params& p, uint64_t u, uint32_t hint) {
+template <class P>
+__device__ __forceinline__ uint32_t find_desc(const P& p, uint64_t u, uint32_t hint) {
   // descriptors are visited in increasing unit order by each warp: gallop from the hint
   uint32_t lo = hint, hi = p.n;  // invariant: d[lo].unit_begin <= u
   if (p.d[lo].unit_begin > u) lo = 0;
@@ -346,8 +352,8 @@ __device__ __forceinline__ uint32_t find_desc(const Params& p, uint64_t u, uint3
   return lo;
 }
 
-template <int K>
-__global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant__ Params p) {
+template <int K, class P>
+__global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant__ P p) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   uint32_t di = 0;
@@ -383,14 +389,14 @@ static int conversion_kind(uint32_t s, uint32_t d) {
 
 static std::atomic<uint64_t> g_launches{0};
 
-typedef void (*KernelFn)(Params);
-static KernelFn kernel_of(int kind) {
+template <class P>
+static auto kernel_of(int kind) -> void (*)(P) {
   switch (kind) {
-    case K_COPY1: return gather_kernel<K_COPY1>;
-    case K_BF16_F16: return gather_kernel<K_BF16_F16>;
-    case K_F32_F16: return gather_kernel<K_F32_F16>;
-    case K_F16_F32: return gather_kernel<K_F16_F32>;
-    default: return gather_kernel<K_BF16_F32>;
+    case K_COPY1: return gather_kernel<K_COPY1, P>;
+    case K_BF16_F16: return gather_kernel<K_BF16_F16, P>;
+    case K_F32_F16: return gather_kernel<K_F32_F16, P>;
+    case K_F16_F32: return gather_kernel<K_F16_F32, P>;
+    default: return gather_kernel<K_BF16_F32, P>;
   }
 }
 
@@ -410,7 +416,7 @@ static const DevInfo& dev_info() {
     cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
     for (int k = 0; k < 5; ++k) {
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of(k), kThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(k), kThreads, 0);
       di.blocks_per_sm[k] = b > 0 ? b : 1;
     }
   }
@@ -469,7 +475,16 @@ static int launch(int kind, Params& p, cudaStream_t stream) {
   const uint64_t want = (p.total_units + kWarps - 1) / kWarps;
   const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind];
   const unsigned grid = (unsigned)(want < cap ? want : cap);
-  kernel_of(kind)<<<grid, kThreads, 0, stream>>>(p);
+  if (p.n <= (uint32_t)kSmallDescs) {
+    SmallParams sp;
+    sp.n = p.n;
+    sp.pad = 0;
+    sp.total_units = p.total_units;
+    for (uint32_t i = 0; i < p.n; ++i) sp.d[i] = p.d[i];
+    kernel_of<SmallParams>(kind)<<<grid, kThreads, 0, stream>>>(sp);
+  } else {
+    kernel_of<Params>(kind)<<<grid, kThreads, 0, stream>>>(p);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HL_ECUDA, "gather launch failed: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);

@@ -146,6 +146,7 @@ struct Slot {
   uint8_t* host = nullptr;
   cudaEvent_t ev = nullptr;
   bool busy = false;
+  void* reg = nullptr;  // HL_IO_MMAP: page-cache range pinned for the in-flight DMA
 };
 struct WorkerRing {
   std::vector<Slot> slots;
@@ -173,6 +174,7 @@ struct FileState {
   int bfd = -1, dfd = -1;  // buffered / O_DIRECT descriptors
   int mode = HL_IO_BUFFERED;
   void* cufh = nullptr;
+  uint8_t* map = nullptr;  // HL_IO_MMAP: read-only shared mapping of the file
   uint64_t size = 0;
 };
 
@@ -185,7 +187,7 @@ struct PlanRun {
   std::mutex err_mu;
   int err_code = HL_OK;
   std::string err_msg;
-  std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0};
+  std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0}, mmap_bytes{0};
   double ring_setup = 0;
   std::mutex setup_mu;
 
@@ -280,6 +282,30 @@ void worker_main(PlanRun* run, uint32_t w) {
         return;
       }
       s.busy = false;
+      if (s.reg) {
+        cudaHostUnregister(s.reg);
+        s.reg = nullptr;
+      }
+    }
+    if (f.mode == HL_IO_MMAP) {
+      // pin the page-cache pages of this chunk in place and DMA them: no CPU copy
+      uint8_t* p = f.map + c.off;
+      uint8_t* a = (uint8_t*)round_down((uint64_t)(uintptr_t)p, kAlign);
+      const uint64_t alen = round_up((uint64_t)(p - a) + c.len, kAlign);
+      cudaError_t e = cudaHostRegister(a, alen, cudaHostRegisterPortable | cudaHostRegisterReadOnly);
+      if (e == cudaSuccess) {
+        e = cudaMemcpyAsync((void*)c.dst, p, c.len, cudaMemcpyHostToDevice, ring.stream);
+        if (e == cudaSuccess) e = cudaEventRecord(s.ev, ring.stream);
+        if (e != cudaSuccess) {
+          run->fail(HL_ECUDA, std::string("H2D copy (mmap): ") + cudaGetErrorString(e));
+          return;
+        }
+        s.reg = a;
+        s.busy = true;
+        run->mmap_bytes += c.len;
+        continue;
+      }
+      cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
     }
     uint64_t head = 0, got = 0;
     int err = 0;
@@ -320,7 +346,13 @@ void worker_main(PlanRun* run, uint32_t w) {
     s.busy = true;
   }
   cudaError_t e = cudaStreamSynchronize(ring.stream);
-  for (auto& s : ring.slots) s.busy = false;
+  for (auto& s : ring.slots) {
+    s.busy = false;
+    if (s.reg) {
+      cudaHostUnregister(s.reg);
+      s.reg = nullptr;
+    }
+  }
   if (e != cudaSuccess) run->fail(HL_ECUDA, std::string("H2D stream: ") + cudaGetErrorString(e));
 }
 
@@ -359,7 +391,7 @@ extern "C" int hl_ctx_create(const hl_config* cfg, hl_ctx** out) {
     delete ctx;
     return set_error(HL_EINVAL, "device %d out of range (%d visible)", d, ndev);
   }
-  if (ctx->cfg.io_mode > HL_IO_CUFILE) {
+  if (ctx->cfg.io_mode > HL_IO_MMAP) {
     delete ctx;
     return set_error(HL_EINVAL, "unknown io_mode %u", cfg->io_mode);
   }
@@ -412,26 +444,46 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
   const double t0 = now_s();
   cudaSetDevice(ctx->cfg.device);
 
-  // split blocks into chunks (block order preserved)
+  // Merge blocks that continue each other (same file, contiguous in the file
+  // and on the device), then cut chunks at absolute multiples of chunk_bytes in
+  // file-offset space: chunk boundaries are page aligned, so O_DIRECT heads and
+  // mmap-pinned page ranges of neighbouring chunks never overlap.
   std::vector<Chunk> chunks;
   std::vector<char> used(n_files, 0);
   uint64_t total = 0;
+  std::vector<Chunk> ranges;
   for (uint32_t b = 0; b < n_blocks; ++b) {
     const hl_block& bl = blocks[b];
     if (bl.file >= n_files) return set_error(HL_EINVAL, "block %u names file %u of %u", b, bl.file, n_files);
     if (bl.len && !bl.dev_dst) return set_error(HL_EINVAL, "block %u has a null destination", b);
     used[bl.file] = 1;
-    for (uint64_t o = 0; o < bl.len; o += ctx->cfg.chunk_bytes) {
-      const uint64_t n = std::min<uint64_t>(ctx->cfg.chunk_bytes, bl.len - o);
-      chunks.push_back({bl.file, bl.file_off + o, n, bl.dev_dst + o});
-    }
     total += bl.len;
+    if (!bl.len) continue;
+    if (!ranges.empty()) {
+      Chunk& r = ranges.back();
+      if (r.file == bl.file && r.off + r.len == bl.file_off && r.dst + r.len == bl.dev_dst) {
+        r.len += bl.len;
+        continue;
+      }
+    }
+    ranges.push_back({bl.file, bl.file_off, bl.len, bl.dev_dst});
+  }
+  const uint64_t cb = ctx->cfg.chunk_bytes;
+  for (const Chunk& r : ranges) {
+    uint64_t o = r.off;
+    const uint64_t end = r.off + r.len;
+    while (o < end) {
+      const uint64_t n = std::min<uint64_t>(round_down(o, cb) + cb, end) - o;
+      chunks.push_back({r.file, o, n, r.dst + (o - r.off)});
+      o += n;
+    }
   }
 
   // open files, pick the read mode per file
   std::vector<FileState> files(n_files);
   auto close_all = [&]() {
     for (auto& f : files) {
+      if (f.map) munmap(f.map, f.size);
       if (f.cufh && g_cufile.handle_deregister) g_cufile.handle_deregister(f.cufh);
       if (f.bfd >= 0) close(f.bfd);
       if (f.dfd >= 0) close(f.dfd);
@@ -457,6 +509,15 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     // so the GDS-shaped backend reads with O_DIRECT instead (HL_FORCE_CUFILE=1
     // keeps cuFile for experiments).
     if (mode == HL_IO_CUFILE && !hl_gds_available() && !getenv("HL_FORCE_CUFILE")) mode = HL_IO_DIRECT;
+    if (mode == HL_IO_BUFFERED && ctx->cfg.io_mode == HL_IO_AUTO && getenv("HL_WARM_MMAP")) mode = HL_IO_MMAP;
+    if (mode == HL_IO_MMAP) {
+      void* m = f.size ? mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0) : MAP_FAILED;
+      if (m == MAP_FAILED) {
+        mode = HL_IO_BUFFERED;
+      } else {
+        f.map = (uint8_t*)m;
+      }
+    }
     if (mode == HL_IO_DIRECT || mode == HL_IO_CUFILE) {
       f.dfd = open(paths[i], O_RDONLY | O_DIRECT | O_CLOEXEC);
       if (f.dfd < 0 && mode == HL_IO_DIRECT) mode = HL_IO_BUFFERED;  // e.g. tmpfs: EINVAL
@@ -506,6 +567,7 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     stats->direct_bytes = run.direct_bytes.load();
     stats->buffered_bytes = run.buffered_bytes.load();
     stats->cufile_bytes = run.cufile_bytes.load();
+    stats->mmap_bytes = run.mmap_bytes.load();
     stats->ring_setup_seconds = run.ring_setup;
     stats->io_mode_used = mode_mask;
   }

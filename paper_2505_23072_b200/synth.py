@@ -96,19 +96,33 @@ ARCHS = {
 }
 
 
-def entries(arch: str) -> list[Entry]:
-    return ARCHS[arch][0]()
+def entries(arch: str, layers: int | None = None) -> list[Entry]:
+    """All tensors, or a prefix of the transformer blocks (embeddings and the
+    final norm / lm_head kept) when ``layers`` is given — the same shapes at a
+    size one GPU and the box's disk can hold for parity tests."""
+    ents = ARCHS[arch][0]()
+    if layers is None:
+        return ents
+
+    def block(name: str) -> int | None:
+        parts = name.split(".")
+        for i, p in enumerate(parts[:-1]):
+            if p in ("layers", "h") and parts[i + 1].isdigit():
+                return int(parts[i + 1])
+        return None
+
+    return [e for e in ents if (block(e[0]) is None or block(e[0]) < layers)]
 
 
 def nbytes(e: Entry) -> int:
     return math.prod(e[2]) * e[1].size_bytes
 
 
-def split_files(arch: str, ents: list[Entry] | None = None) -> list[list[Entry]]:
+def split_files(arch: str, ents: list[Entry] | None = None, max_bytes: int | None = None) -> list[list[Entry]]:
     """HF-style split: greedy fill up to the max shard size (Llama), one file
     per transformer block (Bloom: embeddings / 70 layers / ln_f), or one file."""
     ents = ents if ents is not None else entries(arch)
-    rule = ARCHS[arch][1]
+    rule = ARCHS[arch][1] if max_bytes is None else max_bytes
     if rule is None:
         return [ents]
     if rule == "per-layer":
@@ -193,12 +207,14 @@ def body_pad(ents: list[Entry], header: str) -> int | None:
 
 
 def generate(arch: str, outdir: str | os.PathLike, header: str = "aligned", seed: int = 0,
-             device: str | None = None, files: list[int] | None = None) -> list[Path]:
+             device: str | None = None, files: list[int] | None = None, layers: int | None = None,
+             max_bytes: int | None = None) -> list[Path]:
     """Write the checkpoint; returns the file paths (all of them, even when
-    ``files`` restricts which ones are (re)written)."""
+    ``files`` restricts which ones are (re)written). ``layers`` keeps only the
+    first transformer blocks; ``max_bytes`` overrides the file split size."""
     outdir = Path(outdir)
     outdir.mkdir(parents=True, exist_ok=True)
-    groups = split_files(arch)
+    groups = split_files(arch, entries(arch, layers), max_bytes)
     paths = []
     base = 0
     for fi, ents in enumerate(groups):

@@ -1,0 +1,170 @@
+"""The BASELINE.json configurations as parity cases, at real tensor shapes.
+
+Every tensor (or shard) the loader makes ready is copied back and compared
+byte for byte with the oracle reading the file on the CPU (np.memmap +
+reference slicing, reference.py:38-66; casts through oracle_c.c):
+
+  C1 GPT-2 small fp32, 1 file (0.5 GB): aligned and odd headers, host / simdirect /
+     gds landings, per-key get_tensor and batched get_tensors, copy-time fp16 cast.
+  C2 Llama-2-7B bf16, 2 files (13.5 GB, full size): get_tensor every key.
+  C3 Llama-2-13B bf16 (first 4 blocks, 3.2 GB, 2 files): get_sharded TP=2 and TP=4.
+  C4 Llama-2-70B bf16 (first 2 blocks, 4.5 GB, 3 files, GQA k/v [1024, 8192]): TP=8.
+  C5 Bloom-176B bf16 (embeddings + 1 block + ln_f, 12.1 GB, 3 files): TP=8 with the
+     bf16 -> fp16 cast on the device, cold page cache.
+
+Multi-rank cases run as thread ranks of one ProcessGroup on the single GPU
+(the box has one B200); the NCCL path shares the same pack descriptors.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import run_ranks  # noqa: E402
+from oracle import oracle  # noqa: E402
+from paper_2505_23072_b200 import LoaderConfig, ProcessGroup, SafeTensorsFileLoader, SingleGroup, _native, synth  # noqa: E402
+from paper_2505_23072_b200.format import DType  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DATA = Path(os.environ.get("HL_TEST_DATA", tempfile.gettempdir())) / "hl_configs"
+
+
+def _gen(name, arch, header="aligned", layers=None, max_bytes=None):
+    d = DATA / name
+    if not (d / "READY").exists():
+        synth.generate(arch, d, header=header, device="cuda", layers=layers, max_bytes=max_bytes)
+        (d / "READY").write_text("ok")
+    return sorted(d.glob("*.safetensors"))
+
+
+def _file_views(paths):
+    """key -> (dtype tag, shape, read-only uint8 memmap of the tensor bytes)."""
+    out = {}
+    for p in paths:
+        body, tensors = oracle.read_header(p)
+        mm = np.memmap(p, dtype=np.uint8, mode="r")
+        for k, (dt, shape, b, e) in tensors.items():
+            out[k] = (dt, shape, mm[body + b: body + e])
+    return out
+
+
+def _host(view) -> np.ndarray:
+    return view.torch.reshape(-1).view(torch.uint8).cpu().numpy() if view.nbytes else np.zeros(0, np.uint8)
+
+
+def _expect_shard(dt, shape, raw, dim, world, rank):
+    unit = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[oracle.SIZES[dt]]
+    lo, hi = oracle.shard_ranges(shape[dim], world)[rank]
+    arr = np.asarray(raw).view(unit).reshape(shape)
+    return np.ascontiguousarray(arr[(slice(None),) * dim + (slice(lo, hi),)]).view(np.uint8).reshape(-1)
+
+
+# ------------------------------------------------------------------------ C1
+@pytest.mark.parametrize("header", ["aligned", "odd"])
+@pytest.mark.parametrize("backend", ["host", "simdirect", "gds"])
+def test_c1_gpt2_fp32(header, backend):
+    paths = _gen(f"gpt2-{header}", "gpt2", header)
+    expect = _file_views(paths)
+    assert len(expect) == 148 and sum(v[2].size for v in expect.values()) == 497_759_232
+    loader = SafeTensorsFileLoader(SingleGroup(), backend)
+    loader.add_filenames({0: paths})
+    fb = loader.copy_files_to_device()
+    keys = sorted(expect)
+    half = len(keys) // 2
+    got = {k: fb.get_tensor(k) for k in keys[:half]}
+    got.update(fb.get_tensors(keys[half:]))
+    for k in keys:
+        assert np.array_equal(_host(got[k]), expect[k][2]), k
+    fb.close()
+    loader.close()
+
+
+def test_c1_gpt2_copy_time_cast_to_fp16():
+    paths = _gen("gpt2-odd", "gpt2", "odd")
+    expect = _file_views(paths)
+    loader = SafeTensorsFileLoader(SingleGroup(), "simdirect")
+    loader.add_filenames({0: paths})
+    fb = loader.copy_files_to_device(dtype=torch.float16)
+    for k in ("wte.weight", "h.3.mlp.c_fc.weight", "ln_f.bias"):
+        v = fb.get_tensor(k)
+        assert v.dtype is DType.F16
+        assert _host(v).tobytes() == oracle.convert(expect[k][2].tobytes(), "F32", "F16"), k
+    fb.close()
+
+
+# ------------------------------------------------------------------------ C2
+def test_c2_llama7b_full_get_tensor():
+    paths = _gen("llama2-7b", "llama2-7b")
+    assert len(paths) == 2
+    expect = _file_views(paths)
+    assert len(expect) == 291 and sum(v[2].size for v in expect.values()) == 13_476_831_232
+    loader = SafeTensorsFileLoader(SingleGroup(), "host")
+    loader.add_filenames({0: paths})
+    fb = loader.copy_files_to_device()
+    assert set(loader.last_transfer_stats.io_modes) <= {"buffered", "direct", "mmap"}
+    for k in [e[0] for e in synth.entries("llama2-7b")]:
+        v = fb.get_tensor(k)
+        assert np.array_equal(_host(v), expect[k][2]), k
+        del v
+    fb.close()
+    loader.close()
+
+
+# ------------------------------------------------------------------------ C3 / C4 / C5 (TP)
+def _tp_case(paths, world, dtype=None, backend="host", cold=False):
+    expect = _file_views(paths)
+    mapping = {r: [str(p) for i, p in enumerate(paths) if i % world == r] for r in range(world)}
+    keys = list(expect)
+    if cold:
+        for p in paths:
+            _native.drop_cache(str(p))
+    group = ProcessGroup(world, timeout=300)
+
+    def rank_main(rank):
+        loader = SafeTensorsFileLoader(group, backend, rank=rank)
+        loader.add_filenames(mapping)
+        fb = loader.copy_files_to_device()
+        bad = []
+        for k in keys:
+            dt, shape, raw = expect[k]
+            d = synth.shard_dim(k, shape)
+            v = fb.get_tensor(k, dtype=dtype) if d is None else fb.get_sharded(k, d, dtype=dtype)
+            exp = raw if d is None else _expect_shard(dt, shape, raw, d, world, rank)
+            exp_b = np.asarray(exp)
+            if dtype is not None:
+                exp_b = np.frombuffer(oracle.convert(exp_b.tobytes(), dt, "F16"), np.uint8)
+            if not np.array_equal(_host(v), exp_b):
+                bad.append(k)
+            del v
+        fb.close()
+        loader.close()
+        return bad
+
+    for rank, bad in enumerate(run_ranks(world, rank_main, join_timeout=900)):
+        assert not bad, (rank, bad[:5])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c3_llama13b_tp(world):
+    _tp_case(_gen("llama2-13b-l4", "llama2-13b", layers=4, max_bytes=2_000_000_000), world)
+
+
+def test_c4_llama70b_tp8():
+    paths = _gen("llama2-70b-l2", "llama2-70b", layers=2, max_bytes=2_000_000_000)
+    _tp_case(paths, 8)
+
+
+def test_c5_bloom_tp8_fp16_cold():
+    paths = _gen("bloom-176b-l1", "bloom-176b", layers=1)
+    assert len(paths) == 3
+    _tp_case(paths, 8, dtype=torch.float16, backend="simdirect", cold=True)

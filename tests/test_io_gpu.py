@@ -12,7 +12,7 @@ from paper_2505_23072_b200.errors import IoError  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-MODES = ["buffered", "direct", "auto", "cufile"]
+MODES = ["buffered", "direct", "auto", "cufile", "mmap"]
 
 
 @pytest.fixture(scope="module")
