@@ -49,21 +49,29 @@ enum Kind : uint8_t {
   K_BF16_F32 = 4,
 };
 
-enum Mode : uint8_t { M_VEC = 0, M_ELEM = 1 };
+// M_ROWS   every row's output is a whole number of 16-byte vectors (or the
+//          descriptor is one contiguous row); warp units never cross a row, so
+//          the source of a unit is one contiguous byte range with one alignment.
+// M_PACKED rows of fewer than kMinRowVecs vectors: units span several rows.
+// M_ELEM   anything else (odd row widths, misaligned dst): per element.
+enum Mode : uint8_t { M_ROWS = 0, M_PACKED = 1, M_ELEM = 2 };
 
 struct KDesc {
   uint64_t src;        // byte address of element (0,0)
   uint64_t dst;        // byte address of the contiguous output
   uint64_t src_pitch;  // bytes between source rows
   uint64_t unit_begin; // first global unit of this descriptor
-  uint64_t nvec;       // M_VEC: full 16 B output vectors; M_ELEM: total elements
-  uint64_t row_elems;  // M_ELEM: elements per row; M_VEC: vectors per row (0 = one row)
-  uint32_t tail;       // M_VEC single-row: trailing elements after the last full vector
+  uint64_t nvec;       // M_ROWS/M_PACKED: full 16 B output vectors; M_ELEM: elements
+  uint64_t row_len;    // M_ROWS/M_PACKED: vectors per row; M_ELEM: elements per row
+  uint32_t upr;        // M_ROWS: warp units per row
+  uint32_t tail;       // single-row descriptors: trailing elements after the last vector
   uint8_t kind, mode, ss, ds;  // conversion kind, mode, src/dst element size
+  uint32_t pad;
 };
-static_assert(sizeof(KDesc) == 56, "KDesc layout");
+static_assert(sizeof(KDesc) == 64, "KDesc layout");
 
-constexpr int kMaxDescs = 560;  // 560*56 + 16 = 31376 B < 32764 B param limit
+constexpr int kMaxDescs = 500;  // 500*64 + 16 = 32016 B < 32764 B param limit
+constexpr uint64_t kMinRowVecs = 64;
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kUnroll = 8;
@@ -193,12 +201,14 @@ __device__ __forceinline__ uint4 extract16(uint4 a, uint4 b, uint32_t s) {
   return o;
 }
 
-// Source span of one output vector, NB bytes from an arbitrary address.
+// Source span of one output vector: NB bytes (16 for copies and bf16->f16, 32
+// for f32->f16, 8 for the widening casts) starting at any byte.
 template <int NB>
 struct Span {
   uint4 v[NB >= 16 ? NB / 16 : 1];
 };
 
+// Generic span load (M_PACKED rows): aligned granules + funnel shift.
 template <int NB>
 __device__ __forceinline__ void load_span(const uint8_t* p, Span<NB>& out) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
@@ -227,6 +237,16 @@ __device__ __forceinline__ void load_span(const uint8_t* p, Span<NB>& out) {
       }
     }
   }
+}
+
+__device__ __forceinline__ uint4 shfl_down16(uint4 v) {
+  return make_uint4(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1),
+                    __shfl_down_sync(0xffffffffu, v.z, 1), __shfl_down_sync(0xffffffffu, v.w, 1));
+}
+__device__ __forceinline__ uint64_t shfl_down8(uint64_t v) {
+  const uint32_t lo = __shfl_down_sync(0xffffffffu, (uint32_t)v, 1);
+  const uint32_t hi = __shfl_down_sync(0xffffffffu, (uint32_t)(v >> 32), 1);
+  return ((uint64_t)hi << 32) | lo;
 }
 
 template <int K>
@@ -291,51 +311,144 @@ __device__ __forceinline__ void store_elem(uint8_t* p, uint32_t sz, uint64_t x) 
 }
 
 __device__ __forceinline__ void elem_move(const KDesc& d, uint64_t e) {
-  const uint64_t row = e / d.row_elems, col = e - row * d.row_elems;
+  const uint64_t row = e / d.row_len, col = e - row * d.row_len;
   const uint8_t* s = reinterpret_cast<const uint8_t*>(d.src) + row * d.src_pitch + col * d.ss;
   uint8_t* o = reinterpret_cast<uint8_t*>(d.dst) + e * d.ds;
   store_elem(o, d.ds, convert_scalar(load_elem(s, d.ss), d.kind));
 }
 
-// ---------------------------------------------------------------- vector unit
+// Element path unit (cold: odd row widths, misaligned destinations).
+__device__ __noinline__ void elem_unit(const KDesc& d, uint64_t lu, uint32_t lane) {
+  const uint64_t e0 = lu * kUnitElems;
+  for (uint32_t k = 0; k < kUnroll; ++k) {
+    const uint64_t e = e0 + k * 32 + lane;
+    if (e < d.nvec) elem_move(d, e);
+  }
+}
+
+// ---------------------------------------------------------------- row units
+// One warp makes vectors [0, n) of one row ready: `rsrc` is the source span of
+// vector 0, `rdst` its 16-byte aligned destination. The source is one
+// contiguous range, so its alignment is uniform across the warp.
+//
+// Aligned source: each lane loads its span with G-byte aligned loads (G = 16,
+// or 8 for the 8-byte spans of widening casts), U vectors in flight per lane.
+//
+// Shifted source (realign): lane i loads the W aligned granules that START its
+// span's window, and takes the one granule past it from lane i+1 with a warp
+// shuffle; lane 31 only serves as that neighbour, so an iteration makes 31
+// vectors ready from 32 coalesced granule loads. Every global load is aligned
+// and used once: no L1 re-reads, half the load instructions of a two-load
+// realign, and the same memory-level parallelism as the aligned path.
 template <int K>
-__device__ __forceinline__ void vec_unit(const KDesc& d, uint64_t lu, uint32_t lane) {
+__device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uint32_t n,
+                                         uint32_t lane) {
   constexpr int NB = KindTraits<K>::NB;
-  constexpr int U = (NB == 32) ? kUnroll / 2 : kUnroll;  // keep live registers bounded
+  constexpr int G = NB >= 16 ? 16 : 8;  // granule
+  constexpr int W = NB / G;             // granules per span (1 or 2)
+  constexpr int U = (W == 2) ? kUnroll / 2 : kUnroll;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(rsrc);
+  const uint32_t sh = a & (G - 1);
+  if (sh == 0) {
+    for (uint32_t base = 0; base < n; base += 32 * U) {
+      // one base pointer per lane; the U vectors sit at constant offsets from it
+      const uint8_t* ps = rsrc + (size_t)(base + lane) * NB;
+      uint8_t* pd = rdst + (size_t)(base + lane) * 16;
+      const int32_t left = (int32_t)(n - base) - (int32_t)lane;  // vector k in range iff k*32 < left
+      Span<NB> sp[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (k * 32 < left) {
+          if constexpr (G == 8) {
+            const uint64_t x = ldg8(ps + k * 32 * NB);
+            sp[k].v[0] = make_uint4((uint32_t)x, (uint32_t)(x >> 32), 0, 0);
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) sp[k].v[w] = ldg16(ps + k * 32 * NB + w * 16);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (k * 32 < left) stg16(pd + k * 32 * 16, convert_vec<K>(sp[k]));
+      }
+    }
+    return;
+  }
+  const uint8_t* gb = rsrc - sh;  // aligned start of vector 0's window
+  constexpr int US = U / 2;         // shifted path: half the vectors in flight (shuffles need registers)
+  for (uint32_t base = 0; base < n; base += 31 * US) {
+    const uint8_t* pg = gb + (size_t)(base + lane) * NB;
+    uint8_t* pd = rdst + (size_t)(base + lane) * 16;
+    const int32_t left = (int32_t)(n - base) - (int32_t)lane;  // lane's vector k in range iff k*31 < left
+    if constexpr (G == 8) {
+      uint64_t g[US];
+#pragma unroll
+      for (int k = 0; k < US; ++k) g[k] = (k * 31 <= left) ? ldg8(pg + k * 31 * 8) : 0;  // == : tail granule
+#pragma unroll
+      for (int k = 0; k < US; ++k) {
+        const uint64_t nb = shfl_down8(g[k]);
+        if (lane < 31 && k * 31 < left) {
+          const uint64_t x = (g[k] >> (8 * sh)) | (nb << (64 - 8 * sh));
+          Span<NB> sp;
+          sp.v[0] = make_uint4((uint32_t)x, (uint32_t)(x >> 32), 0, 0);
+          stg16(pd + k * 31 * 16, convert_vec<K>(sp));
+        }
+      }
+    } else {
+      uint4 g[US][W];
+#pragma unroll
+      for (int k = 0; k < US; ++k) {
+        if (k * 31 < left) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) g[k][w] = ldg16(pg + k * 31 * NB + w * 16);
+        } else if (k * 31 == left) {
+          g[k][0] = ldg16(pg + k * 31 * NB);  // the last span's tail granule
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < US; ++k) {
+        const uint4 nb = shfl_down16(g[k][0]);
+        if (lane < 31 && k * 31 < left) {
+          Span<NB> sp;
+          if constexpr (W == 1) {
+            sp.v[0] = extract16(g[k][0], nb, sh);
+          } else {
+            sp.v[0] = extract16(g[k][0], g[k][1], sh);
+            sp.v[1] = extract16(g[k][1], nb, sh);
+          }
+          stg16(pd + k * 31 * 16, convert_vec<K>(sp));
+        }
+      }
+    }
+  }
+}
+
+// Rows shorter than kMinRowVecs vectors: a unit spans several rows; each
+// vector finds its row (M_PACKED, rare for model weights).
+template <int K>
+__device__ __noinline__ void packed_unit(const KDesc& d, uint64_t lu, uint32_t lane) {
+  constexpr int NB = KindTraits<K>::NB;
+  constexpr int U = 2;  // cold path: keep its registers below the hot loop's
   const uint8_t* src = reinterpret_cast<const uint8_t*>(d.src);
   uint8_t* dst = reinterpret_cast<uint8_t*>(d.dst);
   const uint64_t vbeg = lu * kUnitVecs;
   const uint64_t vend = min(vbeg + kUnitVecs, d.nvec);
-  const uint64_t vpr = d.row_elems;  // vectors per row; 0 = single contiguous row
+  const uint64_t vpr = d.row_len;
   for (uint64_t base = vbeg; base < vend; base += 32 * U) {
     Span<NB> sp[U];
-    uint64_t vi[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const uint64_t v = base + k * 32 + lane;
-      vi[k] = v;
       if (v < vend) {
-        uint64_t off;
-        if (vpr == 0) {
-          off = v * NB;
-        } else {
-          const uint64_t row = v / vpr;
-          off = row * d.src_pitch + (v - row * vpr) * NB;
-        }
-        load_span<NB>(src + off, sp[k]);
+        const uint64_t row = v / vpr;
+        load_span<NB>(src + row * d.src_pitch + (v - row * vpr) * NB, sp[k]);
       }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      if (vi[k] < vend) stg16(dst + vi[k] * 16, convert_vec<K>(sp[k]));
-    }
-  }
-  // single-row tail (< 16 bytes of output) is done by the descriptor's last unit
-  if (d.tail && vend == d.nvec && (vbeg < vend || d.nvec == 0)) {
-    if (lane < d.tail) {
-      const uint64_t e = d.nvec * (16 / d.ds) + lane;
-      const uint8_t* s = src + e * d.ss;
-      store_elem(dst + e * d.ds, d.ds, convert_scalar(load_elem(s, d.ss), d.kind));
+      const uint64_t v = base + k * 32 + lane;
+      if (v < vend) stg16(dst + v * 16, convert_vec<K>(sp[k]));
     }
   }
 }
@@ -352,8 +465,31 @@ __device__ __forceinline__ uint32_t find_desc(const P& p, uint64_t u, uint32_t h
   return lo;
 }
 
+// Two kernels per conversion kind, so the hot one carries no cold code (and no
+// call ABI) in its register budget:
+//   row_kernel      M_ROWS descriptors — every model weight, clone, realign, pack;
+//   generic_kernel  M_PACKED rows and M_ELEM elements (odd widths, tails).
 template <int K, class P>
-__global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant__ P p) {
+__global__ void __launch_bounds__(kThreads) row_kernel(const __grid_constant__ P p) {
+  constexpr int NB = KindTraits<K>::NB;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  uint32_t di = 0;
+  for (uint64_t u = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); u < p.total_units; u += nwarps) {
+    di = find_desc(p, u, di);
+    const KDesc& d = p.d[di];
+    const uint32_t lu = (uint32_t)(u - d.unit_begin);  // < 2^32 units (16 TiB) per descriptor
+    const uint32_t row = lu / d.upr;
+    const uint64_t v0 = (uint64_t)(lu - row * d.upr) * kUnitVecs;
+    const uint64_t v1 = min(v0 + kUnitVecs, d.row_len);
+    const uint8_t* rsrc = reinterpret_cast<const uint8_t*>(d.src) + (uint64_t)row * d.src_pitch + v0 * NB;
+    uint8_t* rdst = reinterpret_cast<uint8_t*>(d.dst) + ((uint64_t)row * d.row_len + v0) * 16;
+    row_unit<K>(rsrc, rdst, (uint32_t)(v1 - v0), lane);
+  }
+}
+
+template <int K, class P>
+__global__ void __launch_bounds__(kThreads) generic_kernel(const __grid_constant__ P p) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   uint32_t di = 0;
@@ -361,16 +497,8 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(const __grid_constant_
     di = find_desc(p, u, di);
     const KDesc& d = p.d[di];
     const uint64_t lu = u - d.unit_begin;
-    if (d.mode == M_ELEM) {
-      const uint64_t e0 = lu * kUnitElems;
-#pragma unroll 4
-      for (uint32_t k = 0; k < kUnroll; ++k) {
-        const uint64_t e = e0 + k * 32 + lane;
-        if (e < d.nvec) elem_move(d, e);
-      }
-    } else {
-      vec_unit<K>(d, lu, lane);
-    }
+    if (d.mode == M_PACKED) packed_unit<K>(d, lu, lane);
+    else elem_unit(d, lu, lane);
   }
 }
 
@@ -390,19 +518,19 @@ static int conversion_kind(uint32_t s, uint32_t d) {
 static std::atomic<uint64_t> g_launches{0};
 
 template <class P>
-static auto kernel_of(int kind) -> void (*)(P) {
+static auto kernel_of(int kind, bool rows) -> void (*)(P) {
   switch (kind) {
-    case K_COPY1: return gather_kernel<K_COPY1, P>;
-    case K_BF16_F16: return gather_kernel<K_BF16_F16, P>;
-    case K_F32_F16: return gather_kernel<K_F32_F16, P>;
-    case K_F16_F32: return gather_kernel<K_F16_F32, P>;
-    default: return gather_kernel<K_BF16_F32, P>;
+    case K_COPY1: return rows ? row_kernel<K_COPY1, P> : generic_kernel<K_COPY1, P>;
+    case K_BF16_F16: return rows ? row_kernel<K_BF16_F16, P> : generic_kernel<K_BF16_F16, P>;
+    case K_F32_F16: return rows ? row_kernel<K_F32_F16, P> : generic_kernel<K_F32_F16, P>;
+    case K_F16_F32: return rows ? row_kernel<K_F16_F32, P> : generic_kernel<K_F16_F32, P>;
+    default: return rows ? row_kernel<K_BF16_F32, P> : generic_kernel<K_BF16_F32, P>;
   }
 }
 
 struct DevInfo {
   int sms = 0;
-  int blocks_per_sm[5] = {0, 0, 0, 0, 0};
+  int blocks_per_sm[5][2] = {};
 };
 
 static const DevInfo& dev_info() {
@@ -415,24 +543,28 @@ static const DevInfo& dev_info() {
   if (di.sms == 0) {
     cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
     for (int k = 0; k < 5; ++k) {
-      int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(k), kThreads, 0);
-      di.blocks_per_sm[k] = b > 0 ? b : 1;
+      for (int r = 0; r < 2; ++r) {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(k, r), kThreads, 0);
+        di.blocks_per_sm[k][r] = b > 0 ? b : 1;
+      }
     }
   }
   return di;
 }
 
-// Translate one ABI descriptor into the kernel form; returns units (0 = empty).
-static int make_kdesc(const hl_desc& h, uint32_t i, KDesc& k, uint64_t* units_out) {
-  *units_out = 0;
+// Translate one ABI descriptor into kernel descriptors: the main one, plus an
+// element-path descriptor for the < 16-byte tail of a single-row copy.
+// Returns the number produced (0 = empty descriptor).
+static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units[2], int* count) {
+  *count = 0;
   const int kind = conversion_kind(h.src_dtype, h.dst_dtype);
   if (kind < 0) return set_error(HL_ECONV, "unsupported conversion %u -> %u (descriptor %u)", h.src_dtype, h.dst_dtype, i);
   const uint32_t ss = kSize[h.src_dtype], ds = kSize[h.dst_dtype];
   if (h.rows == 0 || h.row_elems == 0) return HL_OK;
   if (!h.src || !h.dst) return set_error(HL_EINVAL, "descriptor %u: null pointer", i);
   if (h.dst % ds) return set_error(HL_EALIGN, "descriptor %u: dst 0x%llx not aligned to %u", i, (unsigned long long)h.dst, ds);
-  k = KDesc{};
+  KDesc k{};
   k.src = h.src;
   k.dst = h.dst;
   k.kind = (uint8_t)kind;
@@ -446,34 +578,49 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc& k, uint64_t* units_ou
   }
   k.src_pitch = pitch;
   const uint64_t out_row = relems * ds;
-  uint64_t units;
+  auto elem = [&](KDesc e, uint64_t nrows, uint64_t n_per_row) {
+    e.mode = M_ELEM;
+    e.nvec = nrows * n_per_row;
+    e.row_len = n_per_row;
+    out[*count] = e;
+    units[*count] = (e.nvec + kUnitElems - 1) / kUnitElems;
+    ++*count;
+  };
   if (h.dst % 16 == 0 && (rows == 1 || out_row % 16 == 0)) {
-    k.mode = M_VEC;
-    if (rows == 1) {
-      k.nvec = out_row / 16;
-      k.tail = (uint32_t)((out_row % 16) / ds);
-      k.row_elems = 0;
-    } else {
-      k.nvec = rows * (out_row / 16);
-      k.row_elems = out_row / 16;
+    const uint64_t vpr = out_row / 16;
+    if (vpr) {
+      k.row_len = vpr;
+      k.nvec = rows * vpr;
+      if (rows == 1 || vpr >= kMinRowVecs) {
+        k.mode = M_ROWS;
+        k.upr = (uint32_t)((vpr + kUnitVecs - 1) / kUnitVecs);
+        units[*count] = rows * k.upr;
+      } else {
+        k.mode = M_PACKED;
+        units[*count] = (k.nvec + kUnitVecs - 1) / kUnitVecs;
+      }
+      out[(*count)++] = k;
     }
-    units = (k.nvec + kUnitVecs - 1) / kUnitVecs;
-    if (units == 0) units = 1;  // tail-only descriptor
+    const uint64_t tail = rows == 1 ? (out_row % 16) / ds : 0;
+    if (tail) {
+      KDesc t = k;
+      const uint64_t done = vpr * (16 / ds);  // elements covered by the vectors
+      t.src = h.src + done * ss;
+      t.dst = h.dst + done * ds;
+      t.upr = 0;
+      elem(t, 1, tail);
+    }
   } else {
-    k.mode = M_ELEM;
-    k.nvec = rows * relems;
-    k.row_elems = relems;
-    units = (k.nvec + kUnitElems - 1) / kUnitElems;
+    elem(k, rows, relems);
   }
-  *units_out = units;
   return HL_OK;
 }
 
-static int launch(int kind, Params& p, cudaStream_t stream) {
+static int launch(int kind, bool rows, Params& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
   const DevInfo& di = dev_info();
   const uint64_t want = (p.total_units + kWarps - 1) / kWarps;
-  const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind];
+  const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind][rows];
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   if (p.n <= (uint32_t)kSmallDescs) {
     SmallParams sp;
@@ -481,9 +628,9 @@ static int launch(int kind, Params& p, cudaStream_t stream) {
     sp.pad = 0;
     sp.total_units = p.total_units;
     for (uint32_t i = 0; i < p.n; ++i) sp.d[i] = p.d[i];
-    kernel_of<SmallParams>(kind)<<<grid, kThreads, 0, stream>>>(sp);
+    kernel_of<SmallParams>(kind, rows)<<<grid, kThreads, 0, stream>>>(sp);
   } else {
-    kernel_of<Params>(kind)<<<grid, kThreads, 0, stream>>>(p);
+    kernel_of<Params>(kind, rows)<<<grid, kThreads, 0, stream>>>(p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HL_ECUDA, "gather launch failed: %s", cudaGetErrorString(e));
@@ -506,35 +653,38 @@ extern "C" uint64_t hl_kernel_launches(void) { return g_launches.load(); }
 extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
   clear_error();
   if (n && !descs) return set_error(HL_EINVAL, "null descriptor table");
+  KDesc kd[2];
+  uint64_t ku[2];
+  int cnt = 0;
   // validate everything before launching anything
   for (uint32_t i = 0; i < n; ++i) {
-    KDesc k;
-    uint64_t units;
-    int rc = make_kdesc(descs[i], i, k, &units);
+    int rc = make_kdesc(descs[i], i, kd, ku, &cnt);
     if (rc) return rc;
   }
-  static thread_local Params* p = nullptr;  // ~31 KB: keep it off the stack
+  static thread_local Params* p = nullptr;  // ~32 KB: keep it off the stack
   if (!p) p = new Params();
-  // one kernel specialisation per conversion kind present in the batch
+  // one launch per (conversion kind, kernel) present in the batch
   for (int kind = 0; kind < 5; ++kind) {
-    p->n = 0;
-    p->total_units = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-      if (conversion_kind(descs[i].src_dtype, descs[i].dst_dtype) != kind) continue;
-      KDesc k;
-      uint64_t units;
-      make_kdesc(descs[i], i, k, &units);
-      if (units == 0) continue;
-      k.unit_begin = p->total_units;
-      p->d[p->n++] = k;
-      p->total_units += units;
-      if (p->n == (uint32_t)kMaxDescs) {
-        int rc = launch(kind, *p, (cudaStream_t)stream);
-        if (rc) return rc;
+    for (int rows = 1; rows >= 0; --rows) {
+      p->n = 0;
+      p->total_units = 0;
+      for (uint32_t i = 0; i < n; ++i) {
+        if (conversion_kind(descs[i].src_dtype, descs[i].dst_dtype) != kind) continue;
+        make_kdesc(descs[i], i, kd, ku, &cnt);
+        for (int j = 0; j < cnt; ++j) {
+          if ((kd[j].mode == M_ROWS) != (rows == 1)) continue;
+          kd[j].unit_begin = p->total_units;
+          p->d[p->n++] = kd[j];
+          p->total_units += ku[j];
+          if (p->n == (uint32_t)kMaxDescs) {
+            int rc = launch(kind, rows, *p, (cudaStream_t)stream);
+            if (rc) return rc;
+          }
+        }
       }
+      int rc = launch(kind, rows, *p, (cudaStream_t)stream);
+      if (rc) return rc;
     }
-    int rc = launch(kind, *p, (cudaStream_t)stream);
-    if (rc) return rc;
   }
   return HL_OK;
 }

@@ -73,7 +73,7 @@ def test_sm100a_cubin_and_kernel_symbols():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", str(_native.LIB_PATH)], capture_output=True, text=True).stdout
-    assert "gather_kernel" in sass
+    assert "row_kernel" in sass and "generic_kernel" in sass
     assert "LDG.E.128" in sass or "LDG.E.ENL2.128" in sass or re.search(r"LDG\.E\S*\.128", sass)
     assert re.search(r"STG\.E\S*\.128", sass)
 

@@ -155,3 +155,19 @@ def test_launch_counter_moves():
     before = _native.kernel_launches()
     kernels.run([kernels.copy_desc(t.data_ptr(), t.data_ptr() + 512, 100, DType.F32)], dev)
     assert _native.kernel_launches() == before + 1
+
+
+@pytest.mark.parametrize("sdt,ddt", [(10, 10), (1, 1), (10, 9), (11, 9), (9, 11), (10, 11), (7, 7)])
+@pytest.mark.parametrize("shift", [0, 1, 5, 8, 15])
+def test_long_rows_every_alignment(sdt, ddt, shift):
+    """Row units (M_ROWS): many rows, source rows at varying misalignment
+    (pitch not a multiple of 16), row lengths not multiples of 31 or 256
+    vectors: the shifted (shuffle) path and its unit boundaries."""
+    rng = np.random.default_rng(sdt * 100 + shift)
+    ss, ds = SIZES[sdt], SIZES[ddt]
+    row_elems = (16 // ds) * int(rng.choice([64, 100, 257, 513, 1030]))  # whole output vectors per row
+    rows = int(rng.choice([1, 3, 37]))
+    pitch = row_elems * ss + int(rng.choice([0, 3, 8, 24]))
+    src = rng.integers(0, 256, size=shift + rows * pitch + 64, dtype=np.uint8)
+    got, exp = run_both(src, rows * row_elems * ds, [(shift, 0, rows, row_elems, pitch, sdt, ddt)])
+    assert_same(got, exp)
