@@ -396,8 +396,11 @@ def main():
         e0.record()
         loader = SafeTensorsFileLoader(group, args.backend, rank=rank, config=cfg)
         loader.add_filenames(mapping)
+        t1 = time.perf_counter()
         fb = loader.copy_files_to_device()
+        t2 = time.perf_counter()
         outs = retrieve(fb, batched=False)
+        t3 = time.perf_counter()
         checksum = outs[-1].torch.reshape(-1)[:32].view(torch.uint8).cpu()  # D2H read of the result
         e1.record()
         torch.cuda.synchronize()
@@ -405,11 +408,14 @@ def main():
         ms = max(e0.elapsed_time(e1), wall * 1e3)
         stats = loader.last_transfer_stats
         d2h = checksum.numel()
+        phases.append({"add_filenames_ms": (t1 - t0) * 1e3, "copy_files_to_device_ms": (t2 - t1) * 1e3,
+                       "retrieve_enqueue_ms": (t3 - t2) * 1e3, "drain_ms": wall * 1e3 - (t3 - t0) * 1e3})
         del outs
         fb.close()
         loader.close()
         return max_over_ranks(ms), stats, d2h
 
+    phases = []
     clocks = Clocks(local)
     e2e_ms, launches_e2e, io_modes, h2d_bytes, ring = [], 0, set(), 0, 0.0
     for i in range(args.warmup):
@@ -425,6 +431,7 @@ def main():
             h2d_bytes = st.bytes
             ring = max(ring, st.ring_setup_seconds)
     clk = clocks.stop()
+    phase_med = {k: round(statistics.median(p[k] for p in phases[-args.steps:]), 2) for k in phases[-1]}
     e2e_med = statistics.median(e2e_ms)
     e2e_val = job_bytes / (e2e_med / 1e3) / 1e9
 
@@ -465,7 +472,8 @@ def main():
                        "l2": "inputs (13.5 GB) far exceed the 126 MB L2; no flush needed"},
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "seconds_to_ready": round(e2e_med / 1e3, 4),
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h, "page_cache": "warm",
-                    "io_modes": sorted(io_modes), "ring_setup_seconds_first_load": round(ring, 4)},
+                    "io_modes": sorted(io_modes), "ring_setup_seconds_first_load": round(ring, 4),
+                    "phases_ms": phase_med},
             "e2e_cold": cold,
             "roofline": roofline,
             "io_roofline": io,

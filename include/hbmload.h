@@ -139,6 +139,25 @@ int hl_drop_cache(const char* path);
 /* Is GPUDirect Storage (nvidia-fs) usable on this host? 1 yes, 0 no. */
 int hl_gds_available(void);
 
+/* ---- peer memory: the multi-GPU data plane without a collective library ---------------
+ * A rank exports the HBM buffer holding its landed files once; every other rank
+ * imports it and its own hl_gather launch then reads the slice it needs straight
+ * out of the owner's HBM over NVLink (peer loads), slicing and casting on the
+ * way: the transfer and the shard/cast are one kernel (replaces the reference's
+ * broadcast/scatter data movement, collective.py:175-255). Within one process,
+ * hl_enable_peer_access gives the same for device pointers of other GPUs. */
+typedef struct hl_ipc_handle {
+  uint8_t handle[64];  /* cudaIpcMemHandle_t of the allocation containing the pointer */
+  uint64_t offset;     /* byte offset of the pointer inside that allocation           */
+} hl_ipc_handle;
+
+int hl_ipc_export(const void* dev_ptr, hl_ipc_handle* out);
+/* Open (reference counted per allocation) and return base + offset in this process. */
+int hl_ipc_import(const hl_ipc_handle* h, int device, void** out_ptr);
+/* Drop one reference taken by hl_ipc_import (by the pointer it returned). */
+int hl_ipc_release(void* ptr);
+int hl_enable_peer_access(int device, int peer);
+
 /* ---- batched gather / realign / shard / cast ----------------------------------------
  * One descriptor = one strided 2-D copy with optional dtype conversion:
  *   for r in [0, rows): for c in [0, row_elems):

@@ -15,7 +15,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libhbmload.so"
-SOURCES = ["hl_gather.cu", "hl_io.cpp", "hl_api.cpp"]
+SOURCES = ["hl_gather.cu", "hl_io.cpp", "hl_peer.cpp", "hl_api.cpp"]
 HEADERS = ["hl_internal.h", "../../include/hbmload.h"]
 
 NVCC_FLAGS = [

@@ -139,7 +139,11 @@ def gather(descs: list[tuple], stream_ptr: int) -> None:
     """Enqueue ``[(src, dst, rows, row_elems, src_pitch, src_code, dst_code), ...]``."""
     if not descs:
         return
-    lib = load()
+    lib = _lib or load()
+    if len(descs) == 1:
+        arr = hl_desc(*descs[0])
+        check(lib.hl_gather(C.byref(arr), 1, C.c_void_p(stream_ptr)))
+        return
     arr = (hl_desc * len(descs))(*[hl_desc(*d) for d in descs])
     check(lib.hl_gather(arr, len(descs), C.c_void_p(stream_ptr)))
 

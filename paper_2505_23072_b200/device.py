@@ -56,7 +56,7 @@ __all__ = [
 
 DIRECT_ALIGNMENT = 512               # ref device.py:51 (simdirect landing granularity)
 GDS_ALIGNMENT = 4096                 # cuFile / O_DIRECT block granularity
-DEFAULT_HOST_BOUNCE = 16 * 1024 * 1024  # pinned chunk per pread + H2D hop (ref: 160 MiB host bounce)
+DEFAULT_HOST_BOUNCE = 4 * 1024 * 1024  # pinned chunk per pread + H2D hop (ref: 160 MiB host bounce; 4 MiB measured best, profiles/)
 DEFAULT_ALIGN_BOUNCE = 16 * 1024 * 1024  # kept for API parity; the realign kernel needs no bounce
 
 

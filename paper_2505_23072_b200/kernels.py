@@ -62,16 +62,19 @@ def algorithmic_bytes(descs: list[Desc]) -> int:
 
 
 def run(descs: list[Desc], device: torch.device) -> None:
-    """Enqueue the batch on ``device``'s current stream."""
+    """Enqueue the batch on ``device``'s current stream (the launch goes to the
+    stream's device; hl_gather switches to it when the caller's differs)."""
     if not descs:
         return
-    with torch.cuda.device(device):
-        stream = torch.cuda.current_stream(device)
-        if TIMING is None:
-            _native.gather(descs, stream.cuda_stream)
-            return
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+    if torch.cuda.current_device() != device.index:
+        with torch.cuda.device(device):
+            return run(descs, device)
+    stream = torch.cuda.current_stream(device)
+    if TIMING is None:
         _native.gather(descs, stream.cuda_stream)
-        e1.record(stream)
-        TIMING.append((e0, e1, algorithmic_bytes(descs)))
+        return
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _native.gather(descs, stream.cuda_stream)
+    e1.record(stream)
+    TIMING.append((e0, e1, algorithmic_bytes(descs)))

@@ -57,6 +57,7 @@ def main():
     ap.add_argument("--modes", default="buffered,mmap,direct")
     ap.add_argument("--workers", default="4,8,12,16")
     ap.add_argument("--chunks", default="4,16,64")
+    ap.add_argument("--slots", default="3")
     ap.add_argument("--file", default=None)
     args = ap.parse_args()
     if args.file:
@@ -68,13 +69,14 @@ def main():
     size = path.stat().st_size
     dev = torch.empty(size, dtype=torch.uint8, device="cuda")
     _ = path.read_bytes() if size < (1 << 34) else None  # warm
-    for t in (4, 8, 12, 16):
-        print(json.dumps({"probe": "pread_only_to_pinned", "threads": t, "chunk_mb": 16,
-                          "GBps": round(pread_only(path, t, 16 << 20), 2)}), flush=True)
+    if "buffered" in args.modes:
+        for t in (4, 8, 12, 16):
+            print(json.dumps({"probe": "pread_only_to_pinned", "threads": t, "chunk_mb": 16,
+                              "GBps": round(pread_only(path, t, 16 << 20), 2)}), flush=True)
     for mode in args.modes.split(","):
         for w in map(int, args.workers.split(",")):
-            for c in map(int, args.chunks.split(",")):
-                eng = _native.IoEngine(0, workers=w, chunk_bytes=c << 20, io_mode=mode)
+            for c, sl in [(float(c), int(sl)) for c in args.chunks.split(",") for sl in args.slots.split(",")]:
+                eng = _native.IoEngine(0, workers=w, chunk_bytes=int(c * (1 << 20)), slots_per_worker=sl, io_mode=mode)
                 res = []
                 for i in range(3):
                     if mode == "direct":
@@ -83,7 +85,7 @@ def main():
                     if i:
                         res.append(size / st["seconds"] / 1e9)
                 eng.close()
-                print(json.dumps({"mode": mode, "workers": w, "chunk_mb": c, "GBps": round(max(res), 2),
+                print(json.dumps({"mode": mode, "workers": w, "chunk_mb": c, "slots": sl, "GBps": round(max(res), 2),
                                   "modes_used": st["io_modes"], "ring_setup_s": round(st["ring_setup_seconds"], 4)}),
                       flush=True)
                 if mode == "direct" and w >= 8 and c >= 16:

@@ -8,6 +8,6 @@ V=${VARIANTS:-clone,realign,cast,pack8}
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/ncu_launches.csv python tools/kernel_bench.py --variants "$V" --iters 1 \
     > gpurun_out/ncu_launches_stdout.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gather_kernel -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:row_kernel -s 2 -c 1 \
     -o gpurun_out/prof_clone -f python tools/kernel_bench.py --variants clone --iters 1 \
     > gpurun_out/ncu_full_stdout.log 2>&1
