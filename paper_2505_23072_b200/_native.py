@@ -77,6 +77,10 @@ class hl_desc(C.Structure):
     ]
 
 
+class hl_ipc_handle(C.Structure):
+    _fields_ = [("handle", C.c_uint8 * 64), ("offset", C.c_uint64)]
+
+
 # name -> (restype, argtypes): every symbol include/hbmload.h declares
 SIGNATURES = {
     "hl_version": (C.c_char_p, []),
@@ -93,6 +97,10 @@ SIGNATURES = {
     "hl_gds_available": (C.c_int, []),
     "hl_conversion_supported": (C.c_int, [C.c_uint32, C.c_uint32]),
     "hl_gather": (C.c_int, [C.POINTER(hl_desc), C.c_uint32, C.c_void_p]),
+    "hl_ipc_export": (C.c_int, [C.c_void_p, C.POINTER(hl_ipc_handle)]),
+    "hl_ipc_import": (C.c_int, [C.POINTER(hl_ipc_handle), C.c_int, C.POINTER(C.c_void_p)]),
+    "hl_ipc_release": (C.c_int, [C.c_void_p]),
+    "hl_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
     "hl_gather_max_batch": (C.c_uint32, []),
     "hl_kernel_launches": (C.c_uint64, []),
 }
@@ -208,3 +216,33 @@ def drop_cache(path: str) -> None:
 
 def gds_available() -> bool:
     return bool(load().hl_gds_available())
+
+
+def ipc_export(dev_ptr: int) -> tuple[bytes, int]:
+    """(handle bytes, offset) of the allocation holding ``dev_ptr``: picklable."""
+    h = hl_ipc_handle()
+    check(load().hl_ipc_export(C.c_void_p(dev_ptr), C.byref(h)))
+    return bytes(h.handle), int(h.offset)
+
+
+def ipc_import(handle: tuple[bytes, int], device: int) -> int:
+    h = hl_ipc_handle()
+    C.memmove(h.handle, handle[0], 64)
+    h.offset = handle[1]
+    out = C.c_void_p()
+    check(load().hl_ipc_import(C.byref(h), device, C.byref(out)))
+    return int(out.value)
+
+
+def ipc_release(ptr: int) -> None:
+    check(load().hl_ipc_release(C.c_void_p(ptr)))
+
+
+_peer_enabled: set[tuple[int, int]] = set()
+
+
+def enable_peer_access(device: int, peer: int) -> None:
+    if device == peer or (device, peer) in _peer_enabled:
+        return
+    check(load().hl_enable_peer_access(device, peer))
+    _peer_enabled.add((device, peer))

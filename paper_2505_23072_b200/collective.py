@@ -108,14 +108,15 @@ def clone_slice(view, dim: int, lo: int, hi: int, part_shape, pool, name: str, d
 
 
 def _source_ptr(view, device: torch.device) -> int:
-    """Device address of ``view`` readable from ``device``. Same device: the
-    view itself. Another GPU: a peer copy of the region first."""
-    if view.buffer.tensor.device == device:
-        return view.buffer.ptr + view.base_offset, None
-    region = view.buffer.tensor[view.base_offset : view.base_offset + view.nbytes]
-    tmp = torch.empty(view.nbytes + 16, dtype=torch.uint8, device=device)
-    tmp[: view.nbytes].copy_(region)
-    return tmp.data_ptr(), tmp
+    """Device address of ``view`` readable from ``device``. Another GPU of the
+    same process is read in place over NVLink (peer access), so the kernel on
+    the receiving GPU does the transfer and the slice/cast in one pass."""
+    src_dev = view.buffer.tensor.device
+    if src_dev != device:
+        from . import _native
+
+        _native.enable_peer_access(device.index, src_dev.index)
+    return view.buffer.ptr + view.base_offset, None
 
 
 # ------------------------------------------------------------------------ thread group
@@ -292,8 +293,12 @@ class DistGroup:
     """
 
     def __init__(self, group=None, device: torch.device | None = None, check_order: bool = False,
-                 timeout: float = DEFAULT_TIMEOUT):
+                 timeout: float = DEFAULT_TIMEOUT, data_plane: str = "nccl"):
         import torch.distributed as dist
+
+        if data_plane not in ("nccl", "ipc"):
+            raise ValueError(f"unknown data plane {data_plane!r}")
+        self.data_plane = data_plane
 
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed is not initialised")
@@ -310,6 +315,42 @@ class DistGroup:
 
     def rank_ids(self) -> range:
         return range(self.world_size)
+
+    # -- peer-memory data plane ("ipc") --------------------------------------------------
+    def publish(self, buffers: dict[str, int], device_index: int) -> dict[str, int]:
+        """Exchange the HBM addresses of every rank's landed file buffers.
+
+        ``buffers`` maps this rank's file ids to device pointers (bytes already
+        final on the device: the caller synchronised its stream). Returns
+        ``file id -> pointer usable on this rank`` for ALL files: its own as
+        given, every peer's opened through CUDA IPC. One collective per load.
+        """
+        from . import _native
+
+        mine = {f: _native.ipc_export(p) for f, p in buffers.items()}
+        out = dict(buffers)
+        if self.world_size == 1:
+            return out
+        for r, theirs in self.exchange(self.rank, mine).items():
+            if r == self.rank:
+                continue
+            for f, h in theirs.items():
+                out[f] = _native.ipc_import(h, device_index)
+        return out
+
+    def unpublish(self, imported: dict[str, int], own: set[str]) -> None:
+        """Close peer mappings, then wait until every rank did, so owners may
+        free the memory."""
+        from . import _native
+
+        for f, p in imported.items():
+            if f not in own:
+                _native.ipc_release(p)
+        self.barrier()
+
+    def barrier(self) -> None:
+        if self.world_size > 1:
+            self._dist.barrier(group=self.pg)
 
     def _global(self, r: int) -> int:
         return r if self.pg is None else self._dist.get_global_rank(self.pg, r)

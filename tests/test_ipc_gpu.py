@@ -1,0 +1,163 @@
+"""The peer-memory data plane across real processes (DistGroup(data_plane="ipc")).
+
+W processes share the box's one B200 (CUDA IPC works between processes on the
+same device; the control plane is gloo on 127.0.0.1). Every rank lands only
+its own files, publishes the buffer once, and then every get_tensor /
+get_sharded is ONE hl_gather launch per rank reading the owner's HBM through
+the IPC mapping — on a multi-GPU box the same reads travel over NVLink.
+Results are checked against the reference loader's own outputs
+(tests/golden/corpora/expect.json) and the oracle.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import socket
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.multiprocessing as mp  # noqa: E402
+
+from conftest import GOLDEN, ROOT  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CORPORA = GOLDEN / "corpora"
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, job, q):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, job(rank, world)))
+    except BaseException as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, ("error", f"{type(e).__name__}: {e}\n{traceback.format_exc()}")))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, job, timeout=240):
+    port = _port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, job, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, v = q.get(timeout=timeout)
+        res[r] = v
+    for p in procs:
+        p.join(60)
+    for r, v in res.items():
+        if isinstance(v, tuple) and v and v[0] == "error":
+            raise AssertionError(f"rank {r}: {v[1]}")
+    return [res[r] for r in range(world)]
+
+
+def golden_job(rank, world):
+    """Every golden case of this world size through the ipc data plane."""
+    import json
+
+    from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader
+
+    cases = [c for c in json.loads((CORPORA / "expect.json").read_text())["cases"] if c["world"] == world]
+    group = DistGroup(device=torch.device("cuda", 0), data_plane="ipc", check_order=True)
+    out = {}
+    for case in cases:
+        mapping = {int(r): [str(CORPORA / f) for f in fs] for r, fs in case["mapping"].items()}
+        for auto in (True, False):
+            loader = SafeTensorsFileLoader(group, config=LoaderConfig(backend=case["backend"], auto_release=auto))
+            loader.add_filenames(mapping)
+            fb = loader.copy_files_to_device()
+            got = {}
+            for k in sorted(fb.keys()):
+                m = fb.metadata(k)
+                if case["dim"] < len(m.shape) and m.shape[case["dim"]] >= world:
+                    v, kind = fb.get_sharded(k, case["dim"]), "shard"
+                else:
+                    v, kind = fb.get_tensor(k), "full"
+                got[k] = [kind, list(v.shape), hashlib.sha256(v.tobytes()).hexdigest()]
+            fb.close()
+            loader.close()
+            out[(case["id"], auto)] = got == case["ranks"][rank]
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.timeout(600)
+def test_ipc_plane_matches_reference_loader(world):
+    for rank_result in _run(world, golden_job):
+        assert rank_result and all(rank_result.values()), rank_result
+
+
+def features_job(rank, world):
+    """dtype casts, Megatron dims on a larger checkpoint slice, repeated keys
+    (buffer still alive, then from a surviving tensor), stale shards."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2505_23072_b200 import DistGroup, SafeTensorsFileLoader
+    from paper_2505_23072_b200.errors import StaleKey
+    from paper_2505_23072_b200.format import DType, write_file
+
+    d = f"/tmp/hl_ipc_feat_{os.getppid()}"
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(77)
+    files = []
+    for i in range(world):
+        t = {f"l{i}.q": (DType.BF16, (256, 192), rng.integers(0, 256, 256 * 192 * 2, dtype=np.uint8).tobytes()),
+             f"l{i}.o": (DType.F32, (96, 130), rng.integers(0, 256, 96 * 130 * 4, dtype=np.uint8).tobytes()),
+             f"l{i}.n": (DType.BF16, (192,), rng.integers(0, 256, 384, dtype=np.uint8).tobytes())}
+        p = f"{d}/f{i}.safetensors"
+        if rank == 0:
+            with open(p, "wb") as f:
+                f.write(write_file(t, pad_header_to=301 + i))  # odd bodies: realign on simdirect
+        files.append((p, t))
+    torch.distributed.barrier()
+    group = DistGroup(device=torch.device("cuda", 0), data_plane="ipc")
+    loader = SafeTensorsFileLoader(group, "simdirect")
+    loader.add_filenames({r: [files[r][0]] for r in range(world)})
+    fb = loader.copy_files_to_device()
+    ok = {}
+    keep = []
+    for i, (p, t) in enumerate(files):
+        q = fb.get_sharded(f"l{i}.q", 0, dtype=torch.float16)
+        conv = oracle.convert(t[f"l{i}.q"][2], "BF16", "F16")
+        ok[f"q{i}"] = q.tobytes() == oracle.slice_bytes(conv, "F16", (256, 192), 0, world, rank)[1]
+        o = fb.get_sharded(f"l{i}.o", 1)
+        ok[f"o{i}"] = o.tobytes() == oracle.slice_bytes(t[f"l{i}.o"][2], "F32", (96, 130), 1, world, rank)[1]
+        n1 = fb.get_tensor(f"l{i}.n")
+        n2 = fb.get_tensor(f"l{i}.n")  # repeated: served again
+        ok[f"n{i}"] = n1.tobytes() == n2.tobytes() == t[f"l{i}.n"][2]
+        keep.append(n1)
+        try:
+            fb.get_sharded(f"l{i}.o", 1)  # buffer released after its last key: stale
+            ok[f"stale{i}"] = False
+        except StaleKey:
+            ok[f"stale{i}"] = True
+    fb.close()
+    loader.close()
+    return ok
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.timeout(600)
+def test_ipc_plane_casts_dims_repeats(world):
+    for rank_result in _run(world, features_job):
+        assert all(rank_result.values()), rank_result
