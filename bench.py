@@ -409,6 +409,9 @@ def main():
         stats = loader.last_transfer_stats
         d2h = checksum.numel()
         phases.append({"add_filenames_ms": (t1 - t0) * 1e3, "copy_files_to_device_ms": (t2 - t1) * 1e3,
+                       "engine_ms": stats.engine_seconds * 1e3 if stats else 0.0,
+                       "worker_read_s": stats.read_seconds if stats else 0.0,
+                       "worker_wait_s": stats.wait_seconds if stats else 0.0,
                        "retrieve_enqueue_ms": (t3 - t2) * 1e3, "drain_ms": wall * 1e3 - (t3 - t0) * 1e3})
         del outs
         fb.close()

@@ -115,6 +115,8 @@ typedef struct hl_plan_stats {
   double ring_setup_seconds;/* pinned ring allocation charged to this call    */
   uint32_t io_mode_used;    /* bitmask of 1<<hl_io_mode actually used         */
   uint32_t reserved;
+  double read_seconds;      /* sum over workers: time inside pread / cuFileRead / pinning */
+  double wait_seconds;      /* sum over workers: time waiting for a ring slot's DMA      */
 } hl_plan_stats;
 
 int hl_ctx_create(const hl_config* cfg, hl_ctx** out);

@@ -62,6 +62,8 @@ class hl_plan_stats(C.Structure):
         ("ring_setup_seconds", C.c_double),
         ("io_mode_used", C.c_uint32),
         ("reserved", C.c_uint32),
+        ("read_seconds", C.c_double),
+        ("wait_seconds", C.c_double),
     ]
 
 
@@ -184,6 +186,7 @@ class IoEngine:
             "direct_bytes": st.direct_bytes, "buffered_bytes": st.buffered_bytes,
             "cufile_bytes": st.cufile_bytes, "mmap_bytes": st.mmap_bytes,
             "ring_setup_seconds": st.ring_setup_seconds,
+            "read_seconds": st.read_seconds, "wait_seconds": st.wait_seconds,
             "io_modes": modes,
         }
 

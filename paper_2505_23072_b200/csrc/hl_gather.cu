@@ -66,7 +66,7 @@ struct KDesc {
   uint32_t upr;        // M_ROWS: warp units per row
   uint32_t tail;       // single-row descriptors: trailing elements after the last vector
   uint8_t kind, mode, ss, ds;  // conversion kind, mode, src/dst element size
-  uint32_t pad;
+  uint32_t which;              // kernel: 0 generic, 1 + RowClass for M_ROWS
 };
 static_assert(sizeof(KDesc) == 64, "KDesc layout");
 
@@ -340,7 +340,13 @@ __device__ __noinline__ void elem_unit(const KDesc& d, uint64_t lu, uint32_t lan
 // vectors ready from 32 coalesced granule loads. Every global load is aligned
 // and used once: no L1 re-reads, half the load instructions of a two-load
 // realign, and the same memory-level parallelism as the aligned path.
-template <int K>
+// Alignment class of a row-kernel launch (decided on the host per descriptor):
+// every row aligned, every row shifted, or rows that differ (pitch not a
+// multiple of the granule). Separate instantiations keep each hot loop's
+// register budget at 64 (4 resident blocks per SM).
+enum RowClass : int { R_MIXED = 0, R_ALIGNED = 1, R_SHIFTED = 2 };
+
+template <int K, int RC>
 __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uint32_t n,
                                          uint32_t lane) {
   constexpr int NB = KindTraits<K>::NB;
@@ -349,7 +355,7 @@ __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uin
   constexpr int U = (W == 2) ? kUnroll / 2 : kUnroll;
   const uintptr_t a = reinterpret_cast<uintptr_t>(rsrc);
   const uint32_t sh = a & (G - 1);
-  if (sh == 0) {
+  if (RC == R_ALIGNED || (RC == R_MIXED && sh == 0)) {
     for (uint32_t base = 0; base < n; base += 32 * U) {
       // one base pointer per lane; the U vectors sit at constant offsets from it
       const uint8_t* ps = rsrc + (size_t)(base + lane) * NB;
@@ -376,7 +382,7 @@ __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uin
     return;
   }
   const uint8_t* gb = rsrc - sh;  // aligned start of vector 0's window
-  constexpr int US = U / 2;         // shifted path: half the vectors in flight (shuffles need registers)
+  constexpr int US = RC == R_SHIFTED ? U : U / 2;  // the mixed kernel carries both loops
   for (uint32_t base = 0; base < n; base += 31 * US) {
     const uint8_t* pg = gb + (size_t)(base + lane) * NB;
     uint8_t* pd = rdst + (size_t)(base + lane) * 16;
@@ -469,7 +475,7 @@ __device__ __forceinline__ uint32_t find_desc(const P& p, uint64_t u, uint32_t h
 // call ABI) in its register budget:
 //   row_kernel      M_ROWS descriptors — every model weight, clone, realign, pack;
 //   generic_kernel  M_PACKED rows and M_ELEM elements (odd widths, tails).
-template <int K, class P>
+template <int K, class P, int RC>
 __global__ void __launch_bounds__(kThreads) row_kernel(const __grid_constant__ P p) {
   constexpr int NB = KindTraits<K>::NB;
   const uint32_t lane = threadIdx.x & 31;
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) row_kernel(const __grid_constant__ P
     const uint64_t v1 = min(v0 + kUnitVecs, d.row_len);
     const uint8_t* rsrc = reinterpret_cast<const uint8_t*>(d.src) + (uint64_t)row * d.src_pitch + v0 * NB;
     uint8_t* rdst = reinterpret_cast<uint8_t*>(d.dst) + ((uint64_t)row * d.row_len + v0) * 16;
-    row_unit<K>(rsrc, rdst, (uint32_t)(v1 - v0), lane);
+    row_unit<K, RC>(rsrc, rdst, (uint32_t)(v1 - v0), lane);
   }
 }
 
@@ -517,20 +523,31 @@ static int conversion_kind(uint32_t s, uint32_t d) {
 
 static std::atomic<uint64_t> g_launches{0};
 
-template <class P>
-static auto kernel_of(int kind, bool rows) -> void (*)(P) {
-  switch (kind) {
-    case K_COPY1: return rows ? row_kernel<K_COPY1, P> : generic_kernel<K_COPY1, P>;
-    case K_BF16_F16: return rows ? row_kernel<K_BF16_F16, P> : generic_kernel<K_BF16_F16, P>;
-    case K_F32_F16: return rows ? row_kernel<K_F32_F16, P> : generic_kernel<K_F32_F16, P>;
-    case K_F16_F32: return rows ? row_kernel<K_F16_F32, P> : generic_kernel<K_F16_F32, P>;
-    default: return rows ? row_kernel<K_BF16_F32, P> : generic_kernel<K_BF16_F32, P>;
+// which: 0 = generic, 1 + RowClass = row kernel of that class
+template <class P, int K>
+static auto kernel_for(int which) -> void (*)(P) {
+  switch (which) {
+    case 0: return generic_kernel<K, P>;
+    case 1 + R_ALIGNED: return row_kernel<K, P, R_ALIGNED>;
+    case 1 + R_SHIFTED: return row_kernel<K, P, R_SHIFTED>;
+    default: return row_kernel<K, P, R_MIXED>;
   }
 }
+template <class P>
+static auto kernel_of(int kind, int which) -> void (*)(P) {
+  switch (kind) {
+    case K_COPY1: return kernel_for<P, K_COPY1>(which);
+    case K_BF16_F16: return kernel_for<P, K_BF16_F16>(which);
+    case K_F32_F16: return kernel_for<P, K_F32_F16>(which);
+    case K_F16_F32: return kernel_for<P, K_F16_F32>(which);
+    default: return kernel_for<P, K_BF16_F32>(which);
+  }
+}
+constexpr int kWhich = 4;
 
 struct DevInfo {
   int sms = 0;
-  int blocks_per_sm[5][2] = {};
+  int blocks_per_sm[5][kWhich] = {};
 };
 
 static const DevInfo& dev_info() {
@@ -543,10 +560,10 @@ static const DevInfo& dev_info() {
   if (di.sms == 0) {
     cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
     for (int k = 0; k < 5; ++k) {
-      for (int r = 0; r < 2; ++r) {
+      for (int w = 0; w < kWhich; ++w) {
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(k, r), kThreads, 0);
-        di.blocks_per_sm[k][r] = b > 0 ? b : 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(k, w), kThreads, 0);
+        di.blocks_per_sm[k][w] = b > 0 ? b : 1;
       }
     }
   }
@@ -580,6 +597,7 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
   const uint64_t out_row = relems * ds;
   auto elem = [&](KDesc e, uint64_t nrows, uint64_t n_per_row) {
     e.mode = M_ELEM;
+    e.which = 0;
     e.nvec = nrows * n_per_row;
     e.row_len = n_per_row;
     out[*count] = e;
@@ -595,6 +613,9 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
         k.mode = M_ROWS;
         k.upr = (uint32_t)((vpr + kUnitVecs - 1) / kUnitVecs);
         units[*count] = rows * k.upr;
+        const uint64_t g = (kind == K_F16_F32 || kind == K_BF16_F32) ? 8 : 16;  // load granule
+        const bool uniform = rows == 1 || pitch % g == 0;
+        k.which = 1 + (uniform ? (h.src % g == 0 ? R_ALIGNED : R_SHIFTED) : R_MIXED);
       } else {
         k.mode = M_PACKED;
         units[*count] = (k.nvec + kUnitVecs - 1) / kUnitVecs;
@@ -616,11 +637,11 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
   return HL_OK;
 }
 
-static int launch(int kind, bool rows, Params& p, cudaStream_t stream) {
+static int launch(int kind, int which, Params& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
   const DevInfo& di = dev_info();
   const uint64_t want = (p.total_units + kWarps - 1) / kWarps;
-  const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind][rows];
+  const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind][which];
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   if (p.n <= (uint32_t)kSmallDescs) {
     SmallParams sp;
@@ -628,9 +649,9 @@ static int launch(int kind, bool rows, Params& p, cudaStream_t stream) {
     sp.pad = 0;
     sp.total_units = p.total_units;
     for (uint32_t i = 0; i < p.n; ++i) sp.d[i] = p.d[i];
-    kernel_of<SmallParams>(kind, rows)<<<grid, kThreads, 0, stream>>>(sp);
+    kernel_of<SmallParams>(kind, which)<<<grid, kThreads, 0, stream>>>(sp);
   } else {
-    kernel_of<Params>(kind, rows)<<<grid, kThreads, 0, stream>>>(p);
+    kernel_of<Params>(kind, which)<<<grid, kThreads, 0, stream>>>(p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HL_ECUDA, "gather launch failed: %s", cudaGetErrorString(e));
@@ -663,26 +684,26 @@ extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
   }
   static thread_local Params* p = nullptr;  // ~32 KB: keep it off the stack
   if (!p) p = new Params();
-  // one launch per (conversion kind, kernel) present in the batch
+  // one launch per (conversion kind, kernel variant) present in the batch
   for (int kind = 0; kind < 5; ++kind) {
-    for (int rows = 1; rows >= 0; --rows) {
+    for (int which = kWhich - 1; which >= 0; --which) {
       p->n = 0;
       p->total_units = 0;
       for (uint32_t i = 0; i < n; ++i) {
         if (conversion_kind(descs[i].src_dtype, descs[i].dst_dtype) != kind) continue;
         make_kdesc(descs[i], i, kd, ku, &cnt);
         for (int j = 0; j < cnt; ++j) {
-          if ((kd[j].mode == M_ROWS) != (rows == 1)) continue;
+          if ((int)kd[j].which != which) continue;
           kd[j].unit_begin = p->total_units;
           p->d[p->n++] = kd[j];
           p->total_units += ku[j];
           if (p->n == (uint32_t)kMaxDescs) {
-            int rc = launch(kind, rows, *p, (cudaStream_t)stream);
+            int rc = launch(kind, which, *p, (cudaStream_t)stream);
             if (rc) return rc;
           }
         }
       }
-      int rc = launch(kind, rows, *p, (cudaStream_t)stream);
+      int rc = launch(kind, which, *p, (cudaStream_t)stream);
       if (rc) return rc;
     }
   }

@@ -190,6 +190,7 @@ struct PlanRun {
   std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0}, mmap_bytes{0};
   double ring_setup = 0;
   std::mutex setup_mu;
+  std::atomic<uint64_t> read_ns{0}, wait_ns{0};
 
   void fail(int code, const std::string& msg) {
     std::lock_guard<std::mutex> g(err_mu);
@@ -276,7 +277,9 @@ void worker_main(PlanRun* run, uint32_t w) {
     Slot& s = ring.slots[ring.next];
     ring.next = (ring.next + 1) % ring.slots.size();
     if (s.busy) {
+      const double tw = now_s();
       cudaError_t e = cudaEventSynchronize(s.ev);
+      run->wait_ns += (uint64_t)((now_s() - tw) * 1e9);
       if (e != cudaSuccess) {
         run->fail(HL_ECUDA, std::string("H2D completion: ") + cudaGetErrorString(e));
         return;
@@ -307,6 +310,7 @@ void worker_main(PlanRun* run, uint32_t w) {
       }
       cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
     }
+    const double tr = now_s();
     uint64_t head = 0, got = 0;
     int err = 0;
     bool direct = (f.mode == HL_IO_DIRECT && f.dfd >= 0);
@@ -337,6 +341,7 @@ void worker_main(PlanRun* run, uint32_t w) {
       return;
     }
     (direct ? run->direct_bytes : run->buffered_bytes) += c.len;
+    run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
     cudaError_t e = cudaMemcpyAsync((void*)c.dst, s.host + head, c.len, cudaMemcpyHostToDevice, ring.stream);
     if (e == cudaSuccess) e = cudaEventRecord(s.ev, ring.stream);
     if (e != cudaSuccess) {
@@ -570,6 +575,8 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     stats->mmap_bytes = run.mmap_bytes.load();
     stats->ring_setup_seconds = run.ring_setup;
     stats->io_mode_used = mode_mask;
+    stats->read_seconds = run.read_ns.load() * 1e-9;
+    stats->wait_seconds = run.wait_ns.load() * 1e-9;
   }
   if (run.err_code != HL_OK) return set_error(run.err_code, "%s", run.err_msg.c_str());
   return HL_OK;
