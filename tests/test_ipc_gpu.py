@@ -153,6 +153,24 @@ def features_job(rank, world):
             ok[f"stale{i}"] = True
     fb.close()
     loader.close()
+
+    # batched: one pull launch per rank for a whole "layer" of keys
+    from paper_2505_23072_b200 import _native
+
+    loader = SafeTensorsFileLoader(group, "host")
+    loader.add_filenames({r: [files[r][0]] for r in range(world)})
+    fb = loader.copy_files_to_device()
+    keys = [f"l{i}.{x}" for i in range(world) for x in ("q", "o", "n")]
+    dims = {k: (0 if k.endswith("q") else 1) for k in keys if not k.endswith("n")}
+    l0 = _native.kernel_launches()
+    got = fb.get_tensors(keys, dims=dims)
+    ok["batch_launches"] = _native.kernel_launches() - l0 <= 3  # one per conversion kind present
+    for i, (p, t) in enumerate(files):
+        ok[f"bq{i}"] = got[f"l{i}.q"].tobytes() == oracle.slice_bytes(t[f"l{i}.q"][2], "BF16", (256, 192), 0, world, rank)[1]
+        ok[f"bo{i}"] = got[f"l{i}.o"].tobytes() == oracle.slice_bytes(t[f"l{i}.o"][2], "F32", (96, 130), 1, world, rank)[1]
+        ok[f"bn{i}"] = got[f"l{i}.n"].tobytes() == t[f"l{i}.n"][2]
+    fb.close()
+    loader.close()
     return ok
 
 

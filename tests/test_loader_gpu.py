@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 
 from conftest import RankFailure, pad_for_body_residue, random_tensor_set, run_ranks  # noqa: E402
 from oracle import oracle  # noqa: E402
-from paper_2505_23072_b200 import LoaderConfig, ProcessGroup, SafeTensorsFileLoader, SingleGroup  # noqa: E402
+from paper_2505_23072_b200 import LoaderConfig, ProcessGroup, SafeTensorsFileLoader, SingleGroup, _native  # noqa: E402
 from paper_2505_23072_b200.errors import (  # noqa: E402
     BadDim,
     DimTooSmall,
@@ -383,4 +383,23 @@ def test_copy_files_to_device_dtype(tmp_path, rng):
     x = fb.get_tensor("x")
     assert x.dtype is DType.F32 and x.tobytes() == oracle.convert(t["x"][2], "BF16", "F32")
     assert fb.get_tensor("y").tobytes() == t["y"][2]
+    fb.close()
+
+
+def test_get_tensors_batched_matches_per_key(tmp_path, rng):
+    t = random_tensor_set(rng, 12, prefix="b", dtypes=[DType.BF16, DType.F32, DType.U8, DType.I64])
+    p = _write(tmp_path, "b.safetensors", t, pad_for_body_residue(t, 77))
+    keys = sorted(t)
+    dims = {k: 0 for k in keys if len(t[k][1]) >= 1 and t[k][1][0] >= 1}
+    loader = SafeTensorsFileLoader(SingleGroup(), "simdirect")
+    loader.add_filenames({0: [p]})
+    fb = loader.copy_files_to_device()
+    launches = _native.kernel_launches()
+    got = fb.get_tensors(keys, dims=dims)
+    assert _native.kernel_launches() - launches <= 2  # one launch (+1 for odd-width tails)
+    for k in keys:
+        assert got[k].tobytes() == t[k][2] and got[k].shape == t[k][1]
+    assert fb._hosted[str(p)].buffer.released  # all keys consumed: auto-release fired
+    with pytest.raises(BadDim):
+        fb.get_tensors([keys[0]], dims={keys[0]: 9})
     fb.close()
