@@ -44,6 +44,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "model load GB/s & seconds to ready device tensors"
+SHARE_GPU = os.environ.get("HL_SHARE_GPU") == "1"  # exercise the N>1 code path on a 1-GPU box
 ARCH = "llama2-7b"
 
 
@@ -60,6 +61,8 @@ def parse():
     ap.add_argument("--cold", type=int, default=1, help="also time e2e after dropping the page cache")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--quick", action="store_true", help="skip io probes and cpu baseline")
+    ap.add_argument("--data-plane", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1: peer-memory pulls (one hl_gather per rank over NVLink) or NCCL broadcast/scatter")
     return ap.parse_args()
 
 
@@ -252,8 +255,13 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:  # test mode: every rank on cuda:0, gloo control plane (NCCL refuses shared GPUs)
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist)
     from paper_2505_23072_b200 import synth
 
@@ -285,7 +293,7 @@ def main():
 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
-    group = DistGroup() if world > 1 else SingleGroup()
+    group = DistGroup(device=device, data_plane=args.data_plane) if world > 1 else SingleGroup()
     mapping = {r: [str(p) for i, p in enumerate(paths) if i % world == r] for r in range(world)}
     keys = [e[0] for e in ents]
     policy = {e[0]: (synth.shard_dim(e[0], e[2]) if world > 1 else None) for e in ents}
@@ -298,7 +306,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -315,9 +323,11 @@ def main():
 
     job_bytes = sum(ready_bytes_for_rank(r) for r in range(world))
 
+    dims = {k: d for k, d in policy.items() if d is not None}
+
     def retrieve(fb, batched: bool):
-        if world == 1 and batched:
-            return list(fb.get_tensors(keys).values())
+        if batched:
+            return list(fb.get_tensors(keys, dims=dims).values())
         outs = []
         for k in keys:
             d = policy[k]
@@ -339,6 +349,7 @@ def main():
             hosted[p] = _HostedFile(buf, dict(hf.dev_offsets), hf.unconsumed)
         base_loader.config.auto_release = True
         fb = FilesBufferOnDevice(base_loader, hosted)
+        fb._peer, fb._peer_offsets = landed._peer, landed._peer_offsets  # the mapping belongs to `landed`
         return fb
 
     kernels.TIMING = []
@@ -363,7 +374,9 @@ def main():
             k_bytes = sum(nb for _, _, nb in kernels.TIMING)
             k_n = len(kernels.TIMING)
         del outs
-        fb._hosted = {}  # landed buffers are shared across steps
+        torch.cuda.synchronize()
+        barrier()  # every rank is done reading peers' landed buffers
+        fb._hosted, fb._peer = {}, None  # landed buffers (and their mappings) are shared across steps
         fb.close()
     kernels.TIMING = None
     value_ms = statistics.median(vals)
@@ -472,6 +485,7 @@ def main():
                        "tensors": len(ents), "header": args.header, "backend": args.backend,
                        "auto_release": True, "global_batch": 1, "seq_len": 0,
                        "parallelism": f"tp{world}" if world > 1 else "single",
+                       "data_plane": args.data_plane if world > 1 else None,
                        "l2": "inputs (13.5 GB) far exceed the 126 MB L2; no flush needed"},
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "seconds_to_ready": round(e2e_med / 1e3, 4),
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h, "page_cache": "warm",

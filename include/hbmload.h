@@ -117,6 +117,7 @@ typedef struct hl_plan_stats {
   uint32_t reserved;
   double read_seconds;      /* sum over workers: time inside pread / cuFileRead / pinning */
   double wait_seconds;      /* sum over workers: time waiting for a ring slot's DMA      */
+  double submit_seconds;    /* sum over workers: time inside cudaMemcpyAsync/EventRecord */
 } hl_plan_stats;
 
 int hl_ctx_create(const hl_config* cfg, hl_ctx** out);

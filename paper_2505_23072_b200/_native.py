@@ -64,6 +64,7 @@ class hl_plan_stats(C.Structure):
         ("reserved", C.c_uint32),
         ("read_seconds", C.c_double),
         ("wait_seconds", C.c_double),
+        ("submit_seconds", C.c_double),
     ]
 
 
@@ -187,6 +188,7 @@ class IoEngine:
             "cufile_bytes": st.cufile_bytes, "mmap_bytes": st.mmap_bytes,
             "ring_setup_seconds": st.ring_setup_seconds,
             "read_seconds": st.read_seconds, "wait_seconds": st.wait_seconds,
+            "submit_seconds": st.submit_seconds,
             "io_modes": modes,
         }
 

@@ -136,15 +136,21 @@ __device__ __forceinline__ uint32_t np_f16_to_f32(uint32_t h) {
 
 // Vectorised narrowing: two f32 bit patterns -> packed f16x2 (lo in bits 0..15).
 // The hardware RNE conversion equals numpy's for every non-NaN input (overflow
-// to inf, subnormal rounding); NaNs are patched to numpy's payload rule.
-__device__ __forceinline__ uint32_t f32x2_to_f16x2(uint32_t a, uint32_t b) {
+// to inf, subnormal rounding); NaN payloads are numpy's only via the scalar
+// routine, so vectors holding an Inf/NaN (exponent all ones) take it.
+__device__ __forceinline__ uint32_t hw_f32x2_to_f16x2(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(b)), "f"(__uint_as_float(a)));
-  if (((a & 0x7fffffffu) > 0x7f800000u) | ((b & 0x7fffffffu) > 0x7f800000u)) {
-    const uint32_t lo = np_f32_to_f16(a), hi = np_f32_to_f16(b);
-    r = lo | (hi << 16);
-  }
   return r;
+}
+__device__ __forceinline__ uint32_t np_f32x2_to_f16x2(uint32_t a, uint32_t b) {
+  return np_f32_to_f16(a) | (np_f32_to_f16(b) << 16);
+}
+// Bit 31 set iff the f32 exponent is all ones (Inf or NaN): 2 ops per value.
+__device__ __forceinline__ uint32_t special32(uint32_t f) { return ((f | 0x007fffffu) & 0x7fffffffu) + 1u; }
+// Bit 15/31 set iff the bf16 half's exponent is all ones: 2 ops per two values.
+__device__ __forceinline__ uint32_t special_bf16x2(uint32_t w) {
+  return ((w | 0x007f007fu) & 0x7fff7fffu) + 0x00010001u;
 }
 
 // Widening: f16 bits -> f32 bits, hardware exact path with NaN payload patch.
@@ -264,17 +270,35 @@ __device__ __forceinline__ uint4 convert_vec(const Span<KindTraits<K>::NB>& s) {
   } else if constexpr (K == K_BF16_F16) {
     const uint4 v = s.v[0];
     uint4 o;
-    o.x = f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
-    o.y = f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
-    o.z = f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
-    o.w = f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
+    const uint32_t sp = special_bf16x2(v.x) | special_bf16x2(v.y) | special_bf16x2(v.z) | special_bf16x2(v.w);
+    if (__builtin_expect((sp & 0x80008000u) != 0, 0)) {
+      o.x = np_f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
+      o.y = np_f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
+      o.z = np_f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
+      o.w = np_f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
+      return o;
+    }
+    o.x = hw_f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
+    o.y = hw_f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
+    o.z = hw_f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
+    o.w = hw_f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
     return o;
   } else if constexpr (K == K_F32_F16) {
+    const uint4 a = s.v[0], b = s.v[1];
+    const uint32_t sp = special32(a.x) | special32(a.y) | special32(a.z) | special32(a.w) | special32(b.x) |
+                        special32(b.y) | special32(b.z) | special32(b.w);
     uint4 o;
-    o.x = f32x2_to_f16x2(s.v[0].x, s.v[0].y);
-    o.y = f32x2_to_f16x2(s.v[0].z, s.v[0].w);
-    o.z = f32x2_to_f16x2(s.v[1].x, s.v[1].y);
-    o.w = f32x2_to_f16x2(s.v[1].z, s.v[1].w);
+    if (__builtin_expect((sp & 0x80000000u) != 0, 0)) {
+      o.x = np_f32x2_to_f16x2(a.x, a.y);
+      o.y = np_f32x2_to_f16x2(a.z, a.w);
+      o.z = np_f32x2_to_f16x2(b.x, b.y);
+      o.w = np_f32x2_to_f16x2(b.z, b.w);
+      return o;
+    }
+    o.x = hw_f32x2_to_f16x2(a.x, a.y);
+    o.y = hw_f32x2_to_f16x2(a.z, a.w);
+    o.z = hw_f32x2_to_f16x2(b.x, b.y);
+    o.w = hw_f32x2_to_f16x2(b.z, b.w);
     return o;
   } else if constexpr (K == K_F16_F32) {
     const uint32_t a = s.v[0].x, b = s.v[0].y;
@@ -340,6 +364,43 @@ __device__ __noinline__ void elem_unit(const KDesc& d, uint64_t lu, uint32_t lan
 // vectors ready from 32 coalesced granule loads. Every global load is aligned
 // and used once: no L1 re-reads, half the load instructions of a two-load
 // realign, and the same memory-level parallelism as the aligned path.
+// The shifted (realign) loop for 16-byte granules.
+template <int K, int US>
+__device__ __forceinline__ void shifted_rows(const uint8_t* gb, uint8_t* rdst, uint32_t n, uint32_t lane,
+                                             uint32_t sh) {
+  constexpr int NB = KindTraits<K>::NB;
+  constexpr int W = NB / 16;
+  for (uint32_t base = 0; base < n; base += 31 * US) {
+    const uint8_t* pg = gb + (size_t)(base + lane) * NB;
+    uint8_t* pd = rdst + (size_t)(base + lane) * 16;
+    const int32_t left = (int32_t)(n - base) - (int32_t)lane;  // lane's vector k in range iff k*31 < left
+    uint4 g[US][W];
+#pragma unroll
+    for (int k = 0; k < US; ++k) {
+      if (k * 31 < left) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) g[k][w] = ldg16(pg + k * 31 * NB + w * 16);
+      } else if (k * 31 == left) {
+        g[k][0] = ldg16(pg + k * 31 * NB);  // the last span's tail granule
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < US; ++k) {
+      const uint4 nb = shfl_down16(g[k][0]);
+      if (lane < 31 && k * 31 < left) {
+        Span<NB> sp;
+        if constexpr (W == 1) {
+          sp.v[0] = extract16(g[k][0], nb, sh);
+        } else {
+          sp.v[0] = extract16(g[k][0], g[k][1], sh);
+          sp.v[1] = extract16(g[k][1], nb, sh);
+        }
+        stg16(pd + k * 31 * 16, convert_vec<K>(sp));
+      }
+    }
+  }
+}
+
 // Alignment class of a row-kernel launch (decided on the host per descriptor):
 // every row aligned, every row shifted, or rows that differ (pitch not a
 // multiple of the granule). Separate instantiations keep each hot loop's
@@ -383,11 +444,11 @@ __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uin
   }
   const uint8_t* gb = rsrc - sh;  // aligned start of vector 0's window
   constexpr int US = RC == R_SHIFTED ? U : U / 2;  // the mixed kernel carries both loops
-  for (uint32_t base = 0; base < n; base += 31 * US) {
-    const uint8_t* pg = gb + (size_t)(base + lane) * NB;
-    uint8_t* pd = rdst + (size_t)(base + lane) * 16;
-    const int32_t left = (int32_t)(n - base) - (int32_t)lane;  // lane's vector k in range iff k*31 < left
-    if constexpr (G == 8) {
+  if constexpr (G == 8) {
+    for (uint32_t base = 0; base < n; base += 31 * US) {
+      const uint8_t* pg = gb + (size_t)(base + lane) * NB;
+      uint8_t* pd = rdst + (size_t)(base + lane) * 16;
+      const int32_t left = (int32_t)(n - base) - (int32_t)lane;  // lane's vector k in range iff k*31 < left
       uint64_t g[US];
 #pragma unroll
       for (int k = 0; k < US; ++k) g[k] = (k * 31 <= left) ? ldg8(pg + k * 31 * 8) : 0;  // == : tail granule
@@ -401,32 +462,9 @@ __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uin
           stg16(pd + k * 31 * 16, convert_vec<K>(sp));
         }
       }
-    } else {
-      uint4 g[US][W];
-#pragma unroll
-      for (int k = 0; k < US; ++k) {
-        if (k * 31 < left) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) g[k][w] = ldg16(pg + k * 31 * NB + w * 16);
-        } else if (k * 31 == left) {
-          g[k][0] = ldg16(pg + k * 31 * NB);  // the last span's tail granule
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < US; ++k) {
-        const uint4 nb = shfl_down16(g[k][0]);
-        if (lane < 31 && k * 31 < left) {
-          Span<NB> sp;
-          if constexpr (W == 1) {
-            sp.v[0] = extract16(g[k][0], nb, sh);
-          } else {
-            sp.v[0] = extract16(g[k][0], g[k][1], sh);
-            sp.v[1] = extract16(g[k][1], nb, sh);
-          }
-          stg16(pd + k * 31 * 16, convert_vec<K>(sp));
-        }
-      }
     }
+  } else {
+    shifted_rows<K, US>(gb, rdst, n, lane, sh);
   }
 }
 

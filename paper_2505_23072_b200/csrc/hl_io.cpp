@@ -190,7 +190,7 @@ struct PlanRun {
   std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0}, mmap_bytes{0};
   double ring_setup = 0;
   std::mutex setup_mu;
-  std::atomic<uint64_t> read_ns{0}, wait_ns{0};
+  std::atomic<uint64_t> read_ns{0}, wait_ns{0}, submit_ns{0};
 
   void fail(int code, const std::string& msg) {
     std::lock_guard<std::mutex> g(err_mu);
@@ -342,8 +342,10 @@ void worker_main(PlanRun* run, uint32_t w) {
     }
     (direct ? run->direct_bytes : run->buffered_bytes) += c.len;
     run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
+    const double ts = now_s();
     cudaError_t e = cudaMemcpyAsync((void*)c.dst, s.host + head, c.len, cudaMemcpyHostToDevice, ring.stream);
     if (e == cudaSuccess) e = cudaEventRecord(s.ev, ring.stream);
+    run->submit_ns += (uint64_t)((now_s() - ts) * 1e9);
     if (e != cudaSuccess) {
       run->fail(HL_ECUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
       return;
@@ -577,6 +579,7 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     stats->io_mode_used = mode_mask;
     stats->read_seconds = run.read_ns.load() * 1e-9;
     stats->wait_seconds = run.wait_ns.load() * 1e-9;
+    stats->submit_seconds = run.submit_ns.load() * 1e-9;
   }
   if (run.err_code != HL_OK) return set_error(run.err_code, "%s", run.err_msg.c_str());
   return HL_OK;

@@ -86,7 +86,9 @@ def main():
                         res.append(size / st["seconds"] / 1e9)
                 eng.close()
                 print(json.dumps({"mode": mode, "workers": w, "chunk_mb": c, "slots": sl, "GBps": round(max(res), 2),
-                                  "modes_used": st["io_modes"], "ring_setup_s": round(st["ring_setup_seconds"], 4)}),
+                                  "modes_used": st["io_modes"], "ring_setup_s": round(st["ring_setup_seconds"], 4),
+                                  "read_s": round(st["read_seconds"], 3), "wait_s": round(st["wait_seconds"], 3),
+                                  "submit_s": round(st["submit_seconds"], 3), "wall_s": round(st["seconds"], 3)}),
                       flush=True)
                 if mode == "direct" and w >= 8 and c >= 16:
                     break
