@@ -146,17 +146,21 @@ def kernel_launches() -> int:
     return int(load().hl_kernel_launches())
 
 
+def pack(descs: list[tuple]):
+    """The ctypes descriptor table for ``hl_gather`` (built before timing)."""
+    if len(descs) == 1:
+        return C.byref(hl_desc(*descs[0])), 1
+    return (hl_desc * len(descs))(*[hl_desc(*d) for d in descs]), len(descs)
+
+
+def launch(table, n: int, stream_ptr: int) -> None:
+    check((_lib or load()).hl_gather(table, n, C.c_void_p(stream_ptr)))
+
+
 def gather(descs: list[tuple], stream_ptr: int) -> None:
     """Enqueue ``[(src, dst, rows, row_elems, src_pitch, src_code, dst_code), ...]``."""
-    if not descs:
-        return
-    lib = _lib or load()
-    if len(descs) == 1:
-        arr = hl_desc(*descs[0])
-        check(lib.hl_gather(C.byref(arr), 1, C.c_void_p(stream_ptr)))
-        return
-    arr = (hl_desc * len(descs))(*[hl_desc(*d) for d in descs])
-    check(lib.hl_gather(arr, len(descs), C.c_void_p(stream_ptr)))
+    if descs:
+        launch(*pack(descs), stream_ptr)
 
 
 class IoEngine:

@@ -36,6 +36,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "hl_internal.h"
 
@@ -136,21 +137,12 @@ __device__ __forceinline__ uint32_t np_f16_to_f32(uint32_t h) {
 
 // Vectorised narrowing: two f32 bit patterns -> packed f16x2 (lo in bits 0..15).
 // The hardware RNE conversion equals numpy's for every non-NaN input (overflow
-// to inf, subnormal rounding); NaN payloads are numpy's only via the scalar
-// routine, so vectors holding an Inf/NaN (exponent all ones) take it.
+// to inf, subnormal rounding); NaN payloads follow numpy only in the scalar
+// routine, which convert_vec calls for vectors holding a NaN.
 __device__ __forceinline__ uint32_t hw_f32x2_to_f16x2(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(b)), "f"(__uint_as_float(a)));
   return r;
-}
-__device__ __forceinline__ uint32_t np_f32x2_to_f16x2(uint32_t a, uint32_t b) {
-  return np_f32_to_f16(a) | (np_f32_to_f16(b) << 16);
-}
-// Bit 31 set iff the f32 exponent is all ones (Inf or NaN): 2 ops per value.
-__device__ __forceinline__ uint32_t special32(uint32_t f) { return ((f | 0x007fffffu) & 0x7fffffffu) + 1u; }
-// Bit 15/31 set iff the bf16 half's exponent is all ones: 2 ops per two values.
-__device__ __forceinline__ uint32_t special_bf16x2(uint32_t w) {
-  return ((w | 0x007f007fu) & 0x7fff7fffu) + 0x00010001u;
 }
 
 // Widening: f16 bits -> f32 bits, hardware exact path with NaN payload patch.
@@ -263,21 +255,38 @@ template <> struct KindTraits<K_F32_F16> { static constexpr int NB = 32; };
 template <> struct KindTraits<K_F16_F32> { static constexpr int NB = 8; };
 template <> struct KindTraits<K_BF16_F32> { static constexpr int NB = 8; };
 
+// NaN screens (2 ops per 32-bit word): bit 15/31 of the result is set iff the
+// bf16 half / f32 value is a NaN.
+__device__ __forceinline__ uint32_t nan_bf16x2(uint32_t w) { return ((w & 0x7fff7fffu) + 0x007f007fu) & 0x80008000u; }
+__device__ __forceinline__ uint32_t nan_f32(uint32_t f) { return ((f & 0x7fffffffu) + 0x007fffffu) & 0x80000000u; }
+
+// Vectors holding a NaN take numpy's scalar routine out of line, so the hot
+// loop carries neither per-element branches nor the slow path's registers.
+__device__ __noinline__ uint4 np_bf16x8_to_f16x8(uint4 v) {
+  uint4 o;
+  o.x = np_f32_to_f16(v.x << 16) | (np_f32_to_f16(v.x & 0xffff0000u) << 16);
+  o.y = np_f32_to_f16(v.y << 16) | (np_f32_to_f16(v.y & 0xffff0000u) << 16);
+  o.z = np_f32_to_f16(v.z << 16) | (np_f32_to_f16(v.z & 0xffff0000u) << 16);
+  o.w = np_f32_to_f16(v.w << 16) | (np_f32_to_f16(v.w & 0xffff0000u) << 16);
+  return o;
+}
+__device__ __noinline__ uint4 np_f32x8_to_f16x8(uint4 a, uint4 b) {
+  uint4 o;
+  o.x = np_f32_to_f16(a.x) | (np_f32_to_f16(a.y) << 16);
+  o.y = np_f32_to_f16(a.z) | (np_f32_to_f16(a.w) << 16);
+  o.z = np_f32_to_f16(b.x) | (np_f32_to_f16(b.y) << 16);
+  o.w = np_f32_to_f16(b.z) | (np_f32_to_f16(b.w) << 16);
+  return o;
+}
+
 template <int K>
 __device__ __forceinline__ uint4 convert_vec(const Span<KindTraits<K>::NB>& s) {
   if constexpr (K == K_COPY1) {
     return s.v[0];
   } else if constexpr (K == K_BF16_F16) {
     const uint4 v = s.v[0];
+    if (nan_bf16x2(v.x) | nan_bf16x2(v.y) | nan_bf16x2(v.z) | nan_bf16x2(v.w)) return np_bf16x8_to_f16x8(v);
     uint4 o;
-    const uint32_t sp = special_bf16x2(v.x) | special_bf16x2(v.y) | special_bf16x2(v.z) | special_bf16x2(v.w);
-    if (__builtin_expect((sp & 0x80008000u) != 0, 0)) {
-      o.x = np_f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
-      o.y = np_f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
-      o.z = np_f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
-      o.w = np_f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
-      return o;
-    }
     o.x = hw_f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
     o.y = hw_f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
     o.z = hw_f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
@@ -285,16 +294,10 @@ __device__ __forceinline__ uint4 convert_vec(const Span<KindTraits<K>::NB>& s) {
     return o;
   } else if constexpr (K == K_F32_F16) {
     const uint4 a = s.v[0], b = s.v[1];
-    const uint32_t sp = special32(a.x) | special32(a.y) | special32(a.z) | special32(a.w) | special32(b.x) |
-                        special32(b.y) | special32(b.z) | special32(b.w);
+    if (nan_f32(a.x) | nan_f32(a.y) | nan_f32(a.z) | nan_f32(a.w) | nan_f32(b.x) | nan_f32(b.y) | nan_f32(b.z) |
+        nan_f32(b.w))
+      return np_f32x8_to_f16x8(a, b);
     uint4 o;
-    if (__builtin_expect((sp & 0x80000000u) != 0, 0)) {
-      o.x = np_f32x2_to_f16x2(a.x, a.y);
-      o.y = np_f32x2_to_f16x2(a.z, a.w);
-      o.z = np_f32x2_to_f16x2(b.x, b.y);
-      o.w = np_f32x2_to_f16x2(b.z, b.w);
-      return o;
-    }
     o.x = hw_f32x2_to_f16x2(a.x, a.y);
     o.y = hw_f32x2_to_f16x2(a.z, a.w);
     o.z = hw_f32x2_to_f16x2(b.x, b.y);
@@ -712,38 +715,48 @@ extern "C" uint64_t hl_kernel_launches(void) { return g_launches.load(); }
 extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
   clear_error();
   if (n && !descs) return set_error(HL_EINVAL, "null descriptor table");
+  // translate + validate everything once, before launching anything
+  static thread_local std::vector<KDesc> kds;
+  static thread_local std::vector<uint64_t> units;
+  static thread_local std::vector<uint16_t> bucket;  // kind * kWhich + which
+  kds.clear();
+  units.clear();
+  bucket.clear();
   KDesc kd[2];
   uint64_t ku[2];
   int cnt = 0;
-  // validate everything before launching anything
+  uint32_t present = 0;  // bitmask of non-empty buckets
   for (uint32_t i = 0; i < n; ++i) {
     int rc = make_kdesc(descs[i], i, kd, ku, &cnt);
     if (rc) return rc;
+    for (int j = 0; j < cnt; ++j) {
+      const uint16_t b = (uint16_t)(kd[j].kind * kWhich + kd[j].which);
+      kds.push_back(kd[j]);
+      units.push_back(ku[j]);
+      bucket.push_back(b);
+      present |= 1u << b;
+    }
   }
   static thread_local Params* p = nullptr;  // ~32 KB: keep it off the stack
   if (!p) p = new Params();
   // one launch per (conversion kind, kernel variant) present in the batch
-  for (int kind = 0; kind < 5; ++kind) {
-    for (int which = kWhich - 1; which >= 0; --which) {
-      p->n = 0;
-      p->total_units = 0;
-      for (uint32_t i = 0; i < n; ++i) {
-        if (conversion_kind(descs[i].src_dtype, descs[i].dst_dtype) != kind) continue;
-        make_kdesc(descs[i], i, kd, ku, &cnt);
-        for (int j = 0; j < cnt; ++j) {
-          if ((int)kd[j].which != which) continue;
-          kd[j].unit_begin = p->total_units;
-          p->d[p->n++] = kd[j];
-          p->total_units += ku[j];
-          if (p->n == (uint32_t)kMaxDescs) {
-            int rc = launch(kind, which, *p, (cudaStream_t)stream);
-            if (rc) return rc;
-          }
-        }
+  for (int b = 0; b < 5 * kWhich; ++b) {
+    if (!(present & (1u << b))) continue;
+    const int kind = b / kWhich, which = b % kWhich;
+    p->n = 0;
+    p->total_units = 0;
+    for (size_t i = 0; i < kds.size(); ++i) {
+      if (bucket[i] != b) continue;
+      kds[i].unit_begin = p->total_units;
+      p->d[p->n++] = kds[i];
+      p->total_units += units[i];
+      if (p->n == (uint32_t)kMaxDescs) {
+        int rc = launch(kind, which, *p, (cudaStream_t)stream);
+        if (rc) return rc;
       }
-      int rc = launch(kind, which, *p, (cudaStream_t)stream);
-      if (rc) return rc;
     }
+    int rc = launch(kind, which, *p, (cudaStream_t)stream);
+    if (rc) return rc;
   }
   return HL_OK;
 }

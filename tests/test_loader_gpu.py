@@ -396,7 +396,7 @@ def test_get_tensors_batched_matches_per_key(tmp_path, rng):
     fb = loader.copy_files_to_device()
     launches = _native.kernel_launches()
     got = fb.get_tensors(keys, dims=dims)
-    assert _native.kernel_launches() - launches <= 2  # one launch (+1 for odd-width tails)
+    assert _native.kernel_launches() - launches <= 4  # one per kernel variant present (aligned/shifted/mixed/generic)
     for k in keys:
         assert got[k].tobytes() == t[k][2] and got[k].shape == t[k][1]
     assert fb._hosted[str(p)].buffer.released  # all keys consumed: auto-release fired
