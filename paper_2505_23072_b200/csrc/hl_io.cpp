@@ -30,6 +30,7 @@
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/uio.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -311,36 +312,62 @@ void worker_main(PlanRun* run, uint32_t w) {
       cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
     }
     const double tr = now_s();
-    uint64_t head = 0, got = 0;
-    int err = 0;
-    bool direct = (f.mode == HL_IO_DIRECT && f.dfd >= 0);
-    bool ok = false;
-    if (direct) {
-      const uint64_t aoff = round_down(c.off, kAlign);
-      head = c.off - aoff;
-      const uint64_t alen = round_up(head + c.len, kAlign);
-      ok = pread_full(f.dfd, s.host, alen, aoff, &got, &err);
-      if (!ok && err == EINVAL) {  // filesystem refused O_DIRECT after all: buffered
-        direct = false;
-      } else if (ok && got < head + c.len) {
-        run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(aoff + got));
+    // Slot layout: the chunk's bytes start at `head` = off % 4 KiB, so the
+    // O_DIRECT part of any read lands 4 KiB-aligned in the slot.
+    const uint64_t head = c.off % kAlign;
+    uint64_t cached = 0;  // leading bytes served from the page cache
+    if (f.mode == HL_IO_BUFFERED || (f.mode == HL_IO_DIRECT && f.dfd < 0)) {
+      uint64_t got = 0;
+      int err = 0;
+      if (!pread_full(f.bfd, s.host + head, c.len, c.off, &got, &err)) {
+        run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err));
         return;
       }
-    }
-    if (!direct) {
-      head = 0;
-      ok = pread_full(f.bfd, s.host, c.len, c.off, &got, &err);
-      if (ok && got < c.len) {
+      if (got < c.len) {
         run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(c.off + got) + " (" +
                               std::to_string(c.len - got) + " bytes short)");
         return;
       }
+      cached = c.len;
+    } else {
+      if (f.mode == HL_IO_AUTO) {
+        // hybrid: take what the page cache holds without blocking, the rest with O_DIRECT
+        while (cached < c.len) {
+          struct iovec iov = {s.host + head + cached, (size_t)(c.len - cached)};
+          ssize_t n = preadv2(f.bfd, &iov, 1, (off_t)(c.off + cached), RWF_NOWAIT);
+          if (n <= 0) break;  // EAGAIN: not cached (or EOF: caught below)
+          cached += (uint64_t)n;
+        }
+      }
+      if (cached < c.len) {
+        const uint64_t from = c.off + cached;
+        const uint64_t aoff = round_down(from, kAlign);
+        const uint64_t alen = round_up(c.off + c.len, kAlign) - aoff;
+        uint8_t* dst = s.host + (aoff - (c.off - head));  // 4 KiB aligned: aoff >= c.off - head
+        uint64_t got = 0;
+        int err = 0;
+        bool ok = f.dfd >= 0 && pread_full(f.dfd, dst, alen, aoff, &got, &err);
+        if (ok && aoff + got < c.off + c.len) {
+          run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(aoff + got));
+          return;
+        }
+        if (!ok && (f.dfd < 0 || err == EINVAL)) {  // no O_DIRECT on this file system: buffered
+          ok = pread_full(f.bfd, s.host + head + cached, c.len - cached, from, &got, &err);
+          if (ok && got < c.len - cached) {
+            run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(from + got));
+            return;
+          }
+        }
+        if (!ok) {
+          run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(from) + ": " + strerror(err));
+          return;
+        }
+        // an O_DIRECT read of the partial first page rewrote bytes before `from`
+        // with identical file contents: harmless
+        run->direct_bytes += c.len - cached;
+      }
     }
-    if (!ok) {
-      run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err));
-      return;
-    }
-    (direct ? run->direct_bytes : run->buffered_bytes) += c.len;
+    run->buffered_bytes += cached;
     run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
     const double ts = now_s();
     cudaError_t e = cudaMemcpyAsync((void*)c.dst, s.host + head, c.len, cudaMemcpyHostToDevice, ring.stream);
@@ -510,13 +537,11 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     fstat(f.bfd, &st);
     f.size = (uint64_t)st.st_size;
     uint32_t mode = ctx->cfg.io_mode;
-    if (mode == HL_IO_AUTO) mode = residency(f.bfd, f.size) >= 0.5 ? HL_IO_BUFFERED : HL_IO_DIRECT;
     // cuFile only where it is real GPUDirect Storage (nvidia-fs loaded); without
     // it cuFile's compat mode is a slower POSIX bounce path than our own ring,
     // so the GDS-shaped backend reads with O_DIRECT instead (HL_FORCE_CUFILE=1
     // keeps cuFile for experiments).
     if (mode == HL_IO_CUFILE && !hl_gds_available() && !getenv("HL_FORCE_CUFILE")) mode = HL_IO_DIRECT;
-    if (mode == HL_IO_BUFFERED && ctx->cfg.io_mode == HL_IO_AUTO && getenv("HL_WARM_MMAP")) mode = HL_IO_MMAP;
     if (mode == HL_IO_MMAP) {
       void* m = f.size ? mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0) : MAP_FAILED;
       if (m == MAP_FAILED) {
@@ -525,7 +550,7 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
         f.map = (uint8_t*)m;
       }
     }
-    if (mode == HL_IO_DIRECT || mode == HL_IO_CUFILE) {
+    if (mode == HL_IO_AUTO || mode == HL_IO_DIRECT || mode == HL_IO_CUFILE) {
       f.dfd = open(paths[i], O_RDONLY | O_DIRECT | O_CLOEXEC);
       if (f.dfd < 0 && mode == HL_IO_DIRECT) mode = HL_IO_BUFFERED;  // e.g. tmpfs: EINVAL
     }
@@ -576,7 +601,11 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     stats->cufile_bytes = run.cufile_bytes.load();
     stats->mmap_bytes = run.mmap_bytes.load();
     stats->ring_setup_seconds = run.ring_setup;
-    stats->io_mode_used = mode_mask;
+    stats->io_mode_used = (run.buffered_bytes.load() ? 1u << HL_IO_BUFFERED : 0u) |
+                          (run.direct_bytes.load() ? 1u << HL_IO_DIRECT : 0u) |
+                          (run.cufile_bytes.load() ? 1u << HL_IO_CUFILE : 0u) |
+                          (run.mmap_bytes.load() ? 1u << HL_IO_MMAP : 0u);
+    (void)mode_mask;
     stats->read_seconds = run.read_ns.load() * 1e-9;
     stats->wait_seconds = run.wait_ns.load() * 1e-9;
     stats->submit_seconds = run.submit_ns.load() * 1e-9;

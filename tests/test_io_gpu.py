@@ -101,3 +101,27 @@ def test_forced_cufile_compat_mode_in_subprocess(blob, tmp_path):
     if r.returncode != 0:
         pytest.xfail(f"cuFile compat mode unavailable: {r.stderr.strip().splitlines()[-1:]}")
     assert "EQUAL True" in r.stdout, r.stdout + r.stderr
+
+
+def test_auto_mode_is_per_chunk_hybrid(blob):
+    """AUTO reads what the page cache holds (RWF_NOWAIT probe) and the rest with
+    O_DIRECT, per chunk: a half-cached file uses both paths and lands exactly."""
+    path, data = blob
+    _native.drop_cache(str(path))
+    with open(path, "rb") as f:  # warm the first half only
+        f.read(data.size // 2)
+    eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode="auto")
+    dst = torch.zeros(data.size, dtype=torch.uint8, device="cuda")
+    st = eng.execute([str(path)], [(0, 0, 0, data.size, dst.data_ptr())])
+    assert st["buffered_bytes"] > 0 and st["direct_bytes"] > 0, st
+    assert st["buffered_bytes"] + st["direct_bytes"] == data.size
+    assert np.array_equal(dst.cpu().numpy(), data)
+    # unaligned ranges through the hybrid path
+    _native.drop_cache(str(path))
+    rng = np.random.default_rng(9)
+    for _ in range(8):
+        off = int(rng.integers(0, data.size - 1))
+        n = int(rng.integers(1, min(3 << 20, data.size - off)))
+        d2 = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+        eng.execute([str(path)], [(0, 0, off, n, d2.data_ptr())])
+        assert np.array_equal(d2.cpu().numpy()[:n], data[off:off + n])
