@@ -175,7 +175,8 @@ struct FileState {
   int bfd = -1, dfd = -1;  // buffered / O_DIRECT descriptors
   int mode = HL_IO_BUFFERED;
   void* cufh = nullptr;
-  uint8_t* map = nullptr;  // HL_IO_MMAP: read-only shared mapping of the file
+  uint8_t* map = nullptr;    // HL_IO_MMAP: read-only shared mapping of the file
+  uint8_t* probe = nullptr;  // HL_IO_AUTO: mapping used only for mincore residency probes
   uint64_t size = 0;
 };
 
@@ -260,6 +261,7 @@ void worker_main(PlanRun* run, uint32_t w) {
   }
   const auto& chunks = *run->chunks;
   auto& files = *run->files;
+  std::vector<unsigned char> vec;  // mincore scratch
   while (!run->failed.load(std::memory_order_relaxed)) {
     const size_t i = run->cursor.fetch_add(1);
     if (i >= chunks.size()) break;
@@ -330,13 +332,21 @@ void worker_main(PlanRun* run, uint32_t w) {
       }
       cached = c.len;
     } else {
-      if (f.mode == HL_IO_AUTO) {
-        // hybrid: take what the page cache holds without blocking, the rest with O_DIRECT
-        while (cached < c.len) {
-          struct iovec iov = {s.host + head + cached, (size_t)(c.len - cached)};
-          ssize_t n = preadv2(f.bfd, &iov, 1, (off_t)(c.off + cached), RWF_NOWAIT);
-          if (n <= 0) break;  // EAGAIN: not cached (or EOF: caught below)
-          cached += (uint64_t)n;
+      if (f.mode == HL_IO_AUTO && f.probe) {
+        // hybrid: the page-cache-resident prefix of the chunk (mincore: no I/O is
+        // triggered, unlike a RWF_NOWAIT probe whose readahead would race the
+        // O_DIRECT reads) is copied from the cache, the rest read with O_DIRECT
+        const uint64_t p0 = c.off / kAlign, p1 = (c.off + c.len + kAlign - 1) / kAlign;
+        if (vec.size() < p1 - p0) vec.resize(p1 - p0);
+        uint64_t res = 0;
+        if (mincore(f.probe + p0 * kAlign, (p1 - p0) * kAlign, vec.data()) == 0) {
+          while (res < p1 - p0 && (vec[res] & 1)) ++res;
+        }
+        const uint64_t upto = std::min<uint64_t>(c.off + c.len, (p0 + res) * kAlign);
+        if (upto > c.off) {
+          uint64_t got = 0;
+          int err = 0;
+          if (pread_full(f.bfd, s.host + head, upto - c.off, c.off, &got, &err)) cached = got;
         }
       }
       if (cached < c.len) {
@@ -518,6 +528,7 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
   auto close_all = [&]() {
     for (auto& f : files) {
       if (f.map) munmap(f.map, f.size);
+      if (f.probe) munmap(f.probe, f.size);
       if (f.cufh && g_cufile.handle_deregister) g_cufile.handle_deregister(f.cufh);
       if (f.bfd >= 0) close(f.bfd);
       if (f.dfd >= 0) close(f.dfd);
@@ -542,6 +553,10 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     // so the GDS-shaped backend reads with O_DIRECT instead (HL_FORCE_CUFILE=1
     // keeps cuFile for experiments).
     if (mode == HL_IO_CUFILE && !hl_gds_available() && !getenv("HL_FORCE_CUFILE")) mode = HL_IO_DIRECT;
+    if (mode == HL_IO_AUTO && f.size) {
+      void* m = mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0);
+      if (m != MAP_FAILED) f.probe = (uint8_t*)m;
+    }
     if (mode == HL_IO_MMAP) {
       void* m = f.size ? mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0) : MAP_FAILED;
       if (m == MAP_FAILED) {
