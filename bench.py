@@ -61,28 +61,49 @@ def parse():
     ap.add_argument("--cold", type=int, default=1, help="also time e2e after dropping the page cache")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--quick", action="store_true", help="skip io probes and cpu baseline")
+    ap.add_argument("--files", type=int, default=0,
+                    help="re-split the checkpoint into this many files (0: HF split at N=1, N files at N>1)")
     ap.add_argument("--data-plane", default="ipc", choices=["ipc", "nccl"],
                     help="N>1: peer-memory pulls (one hl_gather per rank over NVLink) or NCCL broadcast/scatter")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------------------- data
-def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, dist):
+def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, dist, files: int | None = None):
+    """Generate the synthetic checkpoint once per box (GPU RNG). ``files``
+    re-splits it HF-style into that many roughly equal files (same tensors,
+    same order) so that at N ranks every rank owns file bytes to read."""
     from paper_2505_23072_b200 import synth
 
-    d = Path(data_dir) / f"{arch}-{header}"
+    ents = synth.entries(arch)
+    max_bytes = None
+    if files:
+        # greedy split: shrink the cap until the file count is reached (or cannot shrink further)
+        cap = -(-synth.total_bytes(arch) // files)
+        while len(synth.split_files(arch, ents, cap)) > files:
+            cap = int(cap * 1.02) + 1
+        max_bytes = cap
+    tag = f"{arch}-{header}" + (f"-f{files}" if max_bytes else "")
+    d = Path(data_dir) / tag
     marker = d / "READY"
     if rank == 0 and not marker.exists():
         import torch
 
         t0 = time.time()
-        synth.generate(arch, d, header=header, seed=0, device="cuda" if torch.cuda.is_available() else None)
+        synth.generate(arch, d, header=header, seed=0, device="cuda" if torch.cuda.is_available() else None,
+                       max_bytes=max_bytes)
         os.sync()
         marker.write_text(json.dumps({"seconds": time.time() - t0}))
     if world > 1:
         dist.barrier()
-    groups = synth.split_files(arch)
+    groups = synth.split_files(arch, ents, max_bytes)
     return [d / f"model-{i + 1:05d}-of-{len(groups):05d}.safetensors" for i in range(len(groups))]
+
+
+def synth_split(arch):
+    from paper_2505_23072_b200 import synth
+
+    return synth.split_files(arch)
 
 
 def drop_cache(paths):
@@ -262,7 +283,8 @@ def main():
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist)
+    n_files = args.files if args.files else (None if world == 1 else max(world, len(synth_split(args.arch))))
+    paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist, n_files)
     from paper_2505_23072_b200 import synth
 
     ents = synth.entries(args.arch)
