@@ -137,11 +137,17 @@ __device__ __forceinline__ uint32_t np_f16_to_f32(uint32_t h) {
 
 // Vectorised narrowing: two f32 bit patterns -> packed f16x2 (lo in bits 0..15).
 // The hardware RNE conversion equals numpy's for every non-NaN input (overflow
-// to inf, subnormal rounding); NaN payloads follow numpy only in the scalar
-// routine, which convert_vec calls for vectors holding a NaN.
-__device__ __forceinline__ uint32_t hw_f32x2_to_f16x2(uint32_t a, uint32_t b) {
+// to inf, subnormal rounding); NaNs are patched to numpy's payload rule. (Two
+// alternatives measured slower on the 7B batch, profiles/r01_kernel_bench*:
+// one Inf/NaN screen per vector with the slow path inline, 57% of HBM peak,
+// and out of line, 78%; this per-pair form: 87%.)
+__device__ __forceinline__ uint32_t f32x2_to_f16x2(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(b)), "f"(__uint_as_float(a)));
+  if (((a & 0x7fffffffu) > 0x7f800000u) | ((b & 0x7fffffffu) > 0x7f800000u)) {
+    const uint32_t lo = np_f32_to_f16(a), hi = np_f32_to_f16(b);
+    r = lo | (hi << 16);
+  }
   return r;
 }
 
@@ -255,53 +261,24 @@ template <> struct KindTraits<K_F32_F16> { static constexpr int NB = 32; };
 template <> struct KindTraits<K_F16_F32> { static constexpr int NB = 8; };
 template <> struct KindTraits<K_BF16_F32> { static constexpr int NB = 8; };
 
-// NaN screens (2 ops per 32-bit word): bit 15/31 of the result is set iff the
-// bf16 half / f32 value is a NaN.
-__device__ __forceinline__ uint32_t nan_bf16x2(uint32_t w) { return ((w & 0x7fff7fffu) + 0x007f007fu) & 0x80008000u; }
-__device__ __forceinline__ uint32_t nan_f32(uint32_t f) { return ((f & 0x7fffffffu) + 0x007fffffu) & 0x80000000u; }
-
-// Vectors holding a NaN take numpy's scalar routine out of line, so the hot
-// loop carries neither per-element branches nor the slow path's registers.
-__device__ __noinline__ uint4 np_bf16x8_to_f16x8(uint4 v) {
-  uint4 o;
-  o.x = np_f32_to_f16(v.x << 16) | (np_f32_to_f16(v.x & 0xffff0000u) << 16);
-  o.y = np_f32_to_f16(v.y << 16) | (np_f32_to_f16(v.y & 0xffff0000u) << 16);
-  o.z = np_f32_to_f16(v.z << 16) | (np_f32_to_f16(v.z & 0xffff0000u) << 16);
-  o.w = np_f32_to_f16(v.w << 16) | (np_f32_to_f16(v.w & 0xffff0000u) << 16);
-  return o;
-}
-__device__ __noinline__ uint4 np_f32x8_to_f16x8(uint4 a, uint4 b) {
-  uint4 o;
-  o.x = np_f32_to_f16(a.x) | (np_f32_to_f16(a.y) << 16);
-  o.y = np_f32_to_f16(a.z) | (np_f32_to_f16(a.w) << 16);
-  o.z = np_f32_to_f16(b.x) | (np_f32_to_f16(b.y) << 16);
-  o.w = np_f32_to_f16(b.z) | (np_f32_to_f16(b.w) << 16);
-  return o;
-}
-
 template <int K>
 __device__ __forceinline__ uint4 convert_vec(const Span<KindTraits<K>::NB>& s) {
   if constexpr (K == K_COPY1) {
     return s.v[0];
   } else if constexpr (K == K_BF16_F16) {
     const uint4 v = s.v[0];
-    if (nan_bf16x2(v.x) | nan_bf16x2(v.y) | nan_bf16x2(v.z) | nan_bf16x2(v.w)) return np_bf16x8_to_f16x8(v);
     uint4 o;
-    o.x = hw_f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
-    o.y = hw_f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
-    o.z = hw_f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
-    o.w = hw_f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
+    o.x = f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
+    o.y = f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
+    o.z = f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
+    o.w = f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
     return o;
   } else if constexpr (K == K_F32_F16) {
-    const uint4 a = s.v[0], b = s.v[1];
-    if (nan_f32(a.x) | nan_f32(a.y) | nan_f32(a.z) | nan_f32(a.w) | nan_f32(b.x) | nan_f32(b.y) | nan_f32(b.z) |
-        nan_f32(b.w))
-      return np_f32x8_to_f16x8(a, b);
     uint4 o;
-    o.x = hw_f32x2_to_f16x2(a.x, a.y);
-    o.y = hw_f32x2_to_f16x2(a.z, a.w);
-    o.z = hw_f32x2_to_f16x2(b.x, b.y);
-    o.w = hw_f32x2_to_f16x2(b.z, b.w);
+    o.x = f32x2_to_f16x2(s.v[0].x, s.v[0].y);
+    o.y = f32x2_to_f16x2(s.v[0].z, s.v[0].w);
+    o.z = f32x2_to_f16x2(s.v[1].x, s.v[1].y);
+    o.w = f32x2_to_f16x2(s.v[1].z, s.v[1].w);
     return o;
   } else if constexpr (K == K_F16_F32) {
     const uint32_t a = s.v[0].x, b = s.v[0].y;
@@ -446,7 +423,9 @@ __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uin
     return;
   }
   const uint8_t* gb = rsrc - sh;  // aligned start of vector 0's window
-  constexpr int US = RC == R_SHIFTED ? U : U / 2;  // the mixed kernel carries both loops
+  // in-flight vectors on the shifted path: the mixed kernel carries both loops
+  // and the casts need registers for conversion temporaries
+  constexpr int US = (RC == R_SHIFTED && K == K_COPY1) ? U : U / 2;
   if constexpr (G == 8) {
     for (uint32_t base = 0; base < n; base += 31 * US) {
       const uint8_t* pg = gb + (size_t)(base + lane) * NB;

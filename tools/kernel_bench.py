@@ -33,11 +33,15 @@ from paper_2505_23072_b200.format import DType  # noqa: E402
 def batches(variant: str, src: torch.Tensor, dst: torch.Tensor, ents):
     base_s, base_d = src.data_ptr(), dst.data_ptr()
     descs, so, do = [], 0, 0
-    shift = 1 if variant in ("realign", "castodd") else 0
+    shift = 1 if variant in ("realign", "castodd", "f32f16odd", "f16f32odd") else 0
     for name, dt, shape in ents:
         n = math.prod(shape)
-        if variant == "f32f16":
+        if variant in ("f32f16", "f32f16odd"):
             sdt, ddt = DType.F32, DType.F16
+        elif variant in ("f16f32", "f16f32odd"):
+            sdt, ddt = DType.F16, DType.F32
+        elif variant == "bf16f32":
+            sdt, ddt = DType.BF16, DType.F32
         elif variant in ("cast", "castodd"):
             sdt, ddt = DType.BF16, DType.F16
         else:
@@ -59,7 +63,7 @@ def batches(variant: str, src: torch.Tensor, dst: torch.Tensor, ents):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variants", default="clone,realign,cast,castodd,f32f16,pack8")
+    ap.add_argument("--variants", default="clone,realign,cast,castodd,f32f16,f32f16odd,f16f32,f16f32odd,bf16f32,pack8")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--arch", default="llama2-7b")
     args = ap.parse_args()
@@ -69,7 +73,7 @@ def main():
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     ents = synth.entries(args.arch)
     for variant in args.variants.split(","):
-        if variant == "f32f16":
+        if variant in ("f32f16", "f32f16odd"):
             ents_v = [(n, DType.F32, s) for n, _, s in ents]
         else:
             ents_v = ents
