@@ -151,6 +151,18 @@ __device__ __forceinline__ uint32_t f32x2_to_f16x2(uint32_t a, uint32_t b) {
   return r;
 }
 
+// Two bf16 (one 32-bit word) -> packed f16x2: the same hardware conversion,
+// with the NaN test done on the packed bf16 halves in two ops
+// (bit 15 / 31 of ((w & 0x7fff7fff) + 0x007f007f) is set iff that half is a NaN).
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(w & 0xffff0000u)), "f"(__uint_as_float(w << 16)));
+  if (((w & 0x7fff7fffu) + 0x007f007fu) & 0x80008000u) {
+    r = np_f32_to_f16(w << 16) | (np_f32_to_f16(w & 0xffff0000u) << 16);
+  }
+  return r;
+}
+
 // Widening: f16 bits -> f32 bits, hardware exact path with NaN payload patch.
 __device__ __forceinline__ uint32_t f16_to_f32_bits(uint32_t h) {
   if ((h & 0x7c00u) == 0x7c00u && (h & 0x3ffu)) return ((h & 0x8000u) << 16) | 0x7f800000u | ((h & 0x3ffu) << 13);
@@ -267,12 +279,7 @@ __device__ __forceinline__ uint4 convert_vec(const Span<KindTraits<K>::NB>& s) {
     return s.v[0];
   } else if constexpr (K == K_BF16_F16) {
     const uint4 v = s.v[0];
-    uint4 o;
-    o.x = f32x2_to_f16x2(v.x << 16, v.x & 0xffff0000u);
-    o.y = f32x2_to_f16x2(v.y << 16, v.y & 0xffff0000u);
-    o.z = f32x2_to_f16x2(v.z << 16, v.z & 0xffff0000u);
-    o.w = f32x2_to_f16x2(v.w << 16, v.w & 0xffff0000u);
-    return o;
+    return make_uint4(bf16x2_to_f16x2(v.x), bf16x2_to_f16x2(v.y), bf16x2_to_f16x2(v.z), bf16x2_to_f16x2(v.w));
   } else if constexpr (K == K_F32_F16) {
     uint4 o;
     o.x = f32x2_to_f16x2(s.v[0].x, s.v[0].y);
