@@ -222,17 +222,28 @@ bool pread_full(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got,
   return true;
 }
 
+// Stream + event per slot now; the pinned memory of a slot is allocated the
+// first time the slot is used, so a fresh process starts reading into slot 0
+// while the other slots do not exist yet (their allocation overlaps I/O).
 int ensure_ring(hl_ctx* ctx, WorkerRing& r) {
   if (!r.slots.empty()) return HL_OK;
   cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return set_error(HL_ECUDA, "stream create: %s", cudaGetErrorString(e));
   r.slots.resize(ctx->cfg.slots_per_worker);
   for (auto& s : r.slots) {
-    e = cudaHostAlloc((void**)&s.host, ctx->slot_bytes, cudaHostAllocPortable);
-    if (e != cudaSuccess) return set_error(HL_ENOMEM, "pinned slot of %llu bytes: %s",
-                                           (unsigned long long)ctx->slot_bytes, cudaGetErrorString(e));
     e = cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return set_error(HL_ECUDA, "event create: %s", cudaGetErrorString(e));
+  }
+  return HL_OK;
+}
+
+int ensure_slot(hl_ctx* ctx, Slot& s) {
+  if (s.host) return HL_OK;
+  cudaError_t e = cudaHostAlloc((void**)&s.host, ctx->slot_bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    s.host = nullptr;
+    return set_error(HL_ENOMEM, "pinned slot of %llu bytes: %s", (unsigned long long)ctx->slot_bytes,
+                     cudaGetErrorString(e));
   }
   return HL_OK;
 }
@@ -312,6 +323,18 @@ void worker_main(PlanRun* run, uint32_t w) {
         continue;
       }
       cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
+    }
+    if (!s.host) {
+      const double t0 = now_s();
+      int rc = ensure_slot(ctx, s);
+      {
+        std::lock_guard<std::mutex> g(run->setup_mu);
+        run->ring_setup += now_s() - t0;
+      }
+      if (rc) {
+        run->fail(rc, hl_last_error());
+        return;
+      }
     }
     const double tr = now_s();
     // Slot layout: the chunk's bytes start at `head` = off % 4 KiB, so the
