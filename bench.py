@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip io probes and cpu baseline")
     ap.add_argument("--files", type=int, default=0,
                     help="re-split the checkpoint into this many files (0: HF split at N=1, N files at N>1)")
-    ap.add_argument("--data-plane", default="ipc", choices=["ipc", "nccl"],
+    ap.add_argument("--data-plane", default="auto", choices=["auto", "ipc", "nccl"],
                     help="N>1: peer-memory pulls (one hl_gather per rank over NVLink) or NCCL broadcast/scatter")
     return ap.parse_args()
 
@@ -510,7 +510,7 @@ def main():
                        "tensors": len(ents), "header": args.header, "backend": args.backend,
                        "auto_release": True, "global_batch": 1, "seq_len": 0,
                        "parallelism": f"tp{world}" if world > 1 else "single",
-                       "data_plane": args.data_plane if world > 1 else None,
+                       "data_plane": group.data_plane if world > 1 else None,
                        "l2": "inputs (13.5 GB) far exceed the 126 MB L2; no flush needed"},
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "seconds_to_ready": round(e2e_med / 1e3, 4),
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h, "page_cache": "warm",

@@ -293,12 +293,11 @@ class DistGroup:
     """
 
     def __init__(self, group=None, device: torch.device | None = None, check_order: bool = False,
-                 timeout: float = DEFAULT_TIMEOUT, data_plane: str = "nccl"):
+                 timeout: float = DEFAULT_TIMEOUT, data_plane: str = "auto"):
         import torch.distributed as dist
 
-        if data_plane not in ("nccl", "ipc"):
+        if data_plane not in ("auto", "nccl", "ipc"):
             raise ValueError(f"unknown data plane {data_plane!r}")
-        self.data_plane = data_plane
 
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed is not initialised")
@@ -312,6 +311,14 @@ class DistGroup:
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if self.backend == "nccl" else torch.device("cpu")
         self.device = torch.device(device)
+        if data_plane == "auto":
+            # peer memory (CUDA IPC) needs every rank on one node and on GPUs
+            import socket
+
+            hosts = self.exchange(self.rank, socket.gethostname()) if self.world_size > 1 else {0: ""}
+            one_node = len(set(hosts.values())) == 1
+            data_plane = "ipc" if (one_node and self.device.type == "cuda") else "nccl"
+        self.data_plane = data_plane
 
     def rank_ids(self) -> range:
         return range(self.world_size)
