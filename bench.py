@@ -161,37 +161,57 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def cpu_sample(paths):
-    """Bounded CPU sample: the last file of the checkpoint (3.5 GB for 7B)."""
-    return [paths[-1]]
+def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=None):
+    """The reference's CPU load pipeline (oracle port of aggload's loader) on
+    the FULL workload of this arm: W thread-ranks (the reference's in-process
+    ProcessGroup), files round-robin to ranks, each rank's thread-rule preadv
+    workers land its files (transfer.py:197-201, 305-389), then every rank
+    retrieves every key — an auto-release clone (loader.py:456-461) or its
+    slice along the Megatron dim (collective.py:318-330) — from the owner's
+    host buffer. Returns ready tensor bytes per second over all ranks."""
+    import threading
 
-
-def run_cpu_reference(paths, steps: int, warmup: int):
-    """The reference's CPU load pipeline (oracle port of aggload's loader):
-    thread-rule preadv workers, then auto-release clones of every key."""
     from oracle import oracle
 
-    sample = cpu_sample(paths)
-    keys_bytes = 0
-    times = []
-    workers = oracle.thread_rule(len(sample))
+    mapping = {r: [p for i, p in enumerate(paths) if i % world == r] for r in range(world)}
+    workers = {r: oracle.thread_rule(len(mapping[r])) for r in range(world)}
+    policy = policy or {}
+    times, ready = [], 0
     for i in range(warmup + steps):
         t0 = time.perf_counter()
-        ld = oracle.CpuLoader(sample, workers=workers)
-        ld.copy()
-        nb = 0
-        for k in ld.index:
-            nb += ld.get_tensor(k).nbytes
+        loaders = {r: oracle.CpuLoader(mapping[r], workers=workers[r]) for r in range(world) if mapping[r]}
+        ts = [threading.Thread(target=ld.copy) for ld in loaders.values()]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        owner = {k: ld for ld in loaders.values() for k in ld.index}
+        got = [0] * world
+
+        def retrieve(r):
+            nb = 0
+            for k, ld in owner.items():
+                d = policy.get(k) if world > 1 else None
+                nb += (ld.get_tensor(k) if d is None else ld.get_sharded(k, d, world, r)).nbytes
+            got[r] = nb
+
+        ts = [threading.Thread(target=retrieve, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
         dt = time.perf_counter() - t0
-        del ld
-        keys_bytes = nb
+        del loaders, owner
+        ready = sum(got)
         if i >= warmup:
             times.append(dt)
     t = statistics.median(times)
-    return {"value": keys_bytes / t / 1e9, "unit": "GB/s", "cores": workers, "kind": "port",
-            "seconds": t, "sample": f"{Path(sample[0]).name}: {keys_bytes} tensor bytes, "
-            f"{len(oracle.read_header(sample[0])[1])} tensors, warm page cache, reference thread rule "
-            f"({workers} worker(s) for {len(sample)} file(s)), auto_release clones; host os.cpu_count()={os.cpu_count()}"}
+    threads = max(sum(workers.values()), world)
+    return {"value": ready / t / 1e9, "unit": "GB/s", "cores": threads, "kind": "port", "seconds": t,
+            "sample": f"full workload: {len(paths)} file(s), {ready} ready tensor bytes over {world} rank(s), warm "
+                      f"page cache; reference thread rule per rank ({sorted(set(workers.values()))} preadv "
+                      f"worker(s)), then {world} retrieval thread(s) (auto-release clones"
+                      + (" / Megatron-dim slices" if world > 1 else "") + f"); host os.cpu_count()={os.cpu_count()}"}
 
 
 # ----------------------------------------------------------------------------- io probes
@@ -266,6 +286,16 @@ def _storage_read(path, threads: int = 16, chunk: int = 16 << 20) -> float:
     return size / dt / 1e9
 
 
+def hbm_peak_gbs() -> tuple[float, str]:
+    """Roofline denominator: the driver-measured copy bandwidth, else the
+    fallback B200_PROFILING.md states (6.65 TB/s, an earlier measurement)."""
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(peaks["hbm_gbs"]), "of measured: MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    except (OSError, ValueError, KeyError, TypeError):
+        return 6650.0, "of fallback: B200_PROFILING.md 6.65 TB/s (MEASURED_PEAKS.json absent)"
+
+
 # ----------------------------------------------------------------------------- GPU legs
 def main():
     args = parse()
@@ -293,14 +323,15 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            r = run_cpu_reference(paths, args.steps, max(args.warmup, 1))
+            policy = {e[0]: synth.shard_dim(e[0], e[2]) for e in ents}
+            r = run_cpu_reference(paths, args.steps, max(args.warmup, 1), world, policy)
             line = {"metric": METRIC, "value": round(r["value"], 4), "unit": "GB/s", "n_gpus": args.gpus,
                     "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["seconds"] * 1e3, 1),
                     "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                     "data": "synthetic", "impl": "reference",
-                    "config": {"workload": f"{args.arch} bf16, {len(paths)} files, get_tensor every key "
-                               f"(CPU sample: {Path(cpu_sample(paths)[0]).name})", "global_batch": 1, "seq_len": 0,
-                               "parallelism": "cpu"},
+                    "config": {"workload": f"{args.arch} bf16 synthetic, {len(paths)} files, "
+                               + ("get_tensor every key" if world == 1 else f"TP={world} get_sharded (Megatron dims)"),
+                               "global_batch": 1, "seq_len": 0, "parallelism": f"cpu, {world} thread-rank(s)"},
                     "cpu_baseline": r,
                     "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                             "d2h_bytes_per_step": 0}}
@@ -403,12 +434,7 @@ def main():
     kernels.TIMING = None
     value_ms = statistics.median(vals)
     value = job_bytes / (value_ms / 1e3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except OSError:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_peak, peak_source = hbm_peak_gbs()
     achieved = (k_bytes / max(k_n, 1)) / ((k_ms / max(k_n, 1)) / 1e3) / 1e9 if k_n else None
     traffic = None
     tr_file = ROOT / "profiles" / "ncu_traffic.json"
@@ -499,7 +525,7 @@ def main():
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
                     "traffic": traffic, "kernel": "hl_gather row_kernel<K_COPY1, aligned>",
                     "launches_per_step": k_n, "algorithmic_bytes_per_launch": k_bytes // max(k_n, 1),
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+                    "peak_source": peak_source}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(value_ms, 3), "higher_is_better": True,

@@ -107,3 +107,41 @@ def test_loader_repack_layout_matches_reference_tables(golden_cases):
             else:
                 got, _ = _repack_layout([(k, landing[k], m.dtype, m.nbytes) for k, m in h.tensors.items()])
             assert got == offs, (case["id"], f)
+
+
+def test_engine_team_shares_node_cores(monkeypatch):
+    from paper_2505_23072_b200 import transfer
+
+    monkeypatch.setattr(transfer.os, "sched_getaffinity", lambda pid: set(range(40)))
+    monkeypatch.delenv("LOCAL_WORLD_SIZE", raising=False)
+    assert transfer.engine_team(16) == 16
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    assert transfer.engine_team(16) == 4  # floor(0.8 * 40 / 8)
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "64")
+    assert transfer.engine_team(16) == 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_bench_cpu_reference_leg(tmp_path, rng, world):
+    """bench.py's reference arm (the CPU port of the reference pipeline) counts
+    exactly the ready bytes of the arm's workload: full tensors at W=1,
+    every rank's Megatron-dim slice at W>1."""
+    import bench
+    from paper_2505_23072_b200.format import write_file
+
+    paths, policy, expect = [], {}, 0
+    for f in range(3):
+        tensors = {}
+        for i in range(4):
+            shape = (6 + i, 10)
+            raw = rng.integers(0, 256, int(np.prod(shape)) * 2, dtype=np.uint8).tobytes()
+            name = f"f{f}.t{i}"
+            tensors[name] = (DType.BF16, shape, raw)
+            policy[name] = (None, 0, 1, 0)[i]
+            expect += len(raw) * (world if (world > 1 and policy[name] is None) else 1)
+        p = tmp_path / f"m{f}.safetensors"
+        p.write_bytes(write_file(tensors))
+        paths.append(p)
+    r = bench.run_cpu_reference(paths, steps=1, warmup=0, world=world, policy=policy)
+    assert r["kind"] == "port" and r["cores"] >= world
+    assert f"{expect} ready tensor bytes" in r["sample"]
