@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import struct
 import threading
 from pathlib import Path
 
@@ -146,11 +147,17 @@ def kernel_launches() -> int:
     return int(load().hl_kernel_launches())
 
 
+_DESC = struct.Struct("<5Q2I")  # hl_desc, include/hbmload.h (48 bytes, no padding)
+assert _DESC.size == C.sizeof(hl_desc)
+
+
 def pack(descs: list[tuple]):
-    """The ctypes descriptor table for ``hl_gather`` (built before timing)."""
+    """The descriptor table for ``hl_gather``: one struct.pack per entry into
+    a single buffer (~3x cheaper than building ctypes Structures: this runs on
+    the host before the launch, while the GPU waits)."""
     if len(descs) == 1:
         return C.byref(hl_desc(*descs[0])), 1
-    return (hl_desc * len(descs))(*[hl_desc(*d) for d in descs]), len(descs)
+    return (hl_desc * len(descs)).from_buffer_copy(b"".join([_DESC.pack(*d) for d in descs])), len(descs)
 
 
 def launch(table, n: int, stream_ptr: int) -> None:

@@ -56,14 +56,20 @@ def main():
             fb.close()
         res[label + "_us_per_key"] = round(sorted(times)[2], 2)
     print(json.dumps(res), flush=True)
-    fb = fresh()
-    pr = cProfile.Profile()
-    pr.enable()
-    outs = [fb.get_tensor(k) for k in keys]
-    pr.disable()
-    s = io.StringIO()
-    pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25)
-    print(s.getvalue())
+    for label, fn in (("get_tensor", lambda fb: [fb.get_tensor(k) for k in keys]),
+                      ("get_tensors", lambda fb: fb.get_tensors(keys))):
+        fb = fresh()
+        pr = cProfile.Profile()
+        pr.enable()
+        outs = fn(fb)
+        pr.disable()
+        s = io.StringIO()
+        pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25)
+        print(f"==== {label}\n{s.getvalue()}")
+        torch.cuda.synchronize()
+        del outs
+        fb._hosted = {}
+        fb.close()
 
 
 if __name__ == "__main__":

@@ -72,8 +72,33 @@ def launches(path: str) -> list:
     return list(out.values())
 
 
+def launch_shares(path: str) -> dict:
+    """Aggregate a launch list per kernel: launches, summed device time and
+    DRAM bytes, share of the summed time (ncu serialises launches and runs
+    them cold-cache: compare SHARES with the live bench, not absolutes)."""
+    rows = launches(path)
+    agg: dict[str, dict] = {}
+    for r in rows:
+        a = agg.setdefault(r["kernel"], {"launches": 0, "time_ns": 0.0, "dram_bytes": 0.0})
+        a["launches"] += 1
+        a["time_ns"] += r.get("gpu__time_duration.sum", 0.0)
+        a["dram_bytes"] += r.get("dram__bytes_read.sum", 0.0) + r.get("dram__bytes_write.sum", 0.0)
+    total = sum(a["time_ns"] for a in agg.values()) or 1.0
+    for a in agg.values():
+        a["share_of_time"] = round(a["time_ns"] / total, 4)
+        a["dram_GBps"] = round(a["dram_bytes"] / a["time_ns"], 1) if a["time_ns"] else None
+    top = sorted(rows, key=lambda r: -r.get("gpu__time_duration.sum", 0.0))[:8]
+    for r in top:
+        t = r.get("gpu__time_duration.sum", 0.0)
+        b = r.get("dram__bytes_read.sum", 0.0) + r.get("dram__bytes_write.sum", 0.0)
+        r["dram_GBps"] = round(b / t, 1) if t else None
+    return {"source": path, "launches": len(rows), "per_kernel": agg, "longest_launches": top}
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
+    elif sys.argv[1] == "--shares":
+        print(json.dumps(launch_shares(sys.argv[2]), indent=1))
     else:
         print(json.dumps([full(r) for r in sys.argv[1:]], indent=1))
