@@ -60,7 +60,9 @@ def parse():
     ap.add_argument("--data-dir", default=os.environ.get("HL_BENCH_DIR", "/tmp/hl_bench"))
     ap.add_argument("--cold", type=int, default=1, help="also time e2e after dropping the page cache")
     ap.add_argument("--cpu-baseline", type=int, default=1)
-    ap.add_argument("--quick", action="store_true", help="skip io probes and cpu baseline")
+    ap.add_argument("--quick", action="store_true", help="skip io probes, cpu and library baselines")
+    ap.add_argument("--baselines", type=int, default=1,
+                    help="also time upstream fastsafetensors and safetensors on the same files (N=1)")
     ap.add_argument("--files", type=int, default=0,
                     help="re-split the checkpoint into this many files (0: HF split at N=1, N files at N>1)")
     ap.add_argument("--data-plane", default="auto", choices=["auto", "ipc", "nccl"],
@@ -104,6 +106,33 @@ def synth_split(arch):
     from paper_2505_23072_b200 import synth
 
     return synth.split_files(arch)
+
+
+def warm_cache(paths, threads: int = 16, chunk: int = 64 << 20) -> None:
+    """Pull the files back into the page cache with buffered reads (the
+    engine's O_DIRECT reads of a cold file do not populate it)."""
+    import threading
+
+    work = [(str(p), off) for p in paths for off in range(0, os.path.getsize(p), chunk)]
+    lock = threading.Lock()
+
+    def run():
+        while True:
+            with lock:
+                if not work:
+                    return
+                path, off = work.pop()
+            fd = os.open(path, os.O_RDONLY)
+            try:
+                os.pread(fd, chunk, off)
+            finally:
+                os.close(fd)
+
+    ts = [threading.Thread(target=run) for _ in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
 
 
 def drop_cache(paths):
@@ -284,6 +313,64 @@ def _storage_read(path, threads: int = 16, chunk: int = 16 << 20) -> float:
     dt = time.perf_counter() - t0
     os.close(fd)
     return size / dt / 1e9
+
+
+def library_baselines(paths, device_index: int, tensor_bytes: int, steps: int = 3) -> dict:
+    """Same files, same box, warm page cache, every key ready on the GPU
+    (median of ``steps`` after one warm-up): the paper's own implementation
+    (upstream fastsafetensors 0.3.1 from the image, GDS off since the box has
+    no nvidia-fs: its pread + bounce-buffer path; get_tensor returns views)
+    and the paper's baseline (safetensors ``load_file(device="cuda")``)."""
+    import torch
+
+    dev = f"cuda:{device_index}"
+    out = {}
+
+    def timed(fn, n):
+        ts = []
+        for i in range(n + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            if i:
+                ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    try:
+        import fastsafetensors
+        from fastsafetensors import SafeTensorsFileLoader as FstLoader
+
+        def fst():
+            ld = FstLoader(None, dev, nogds=True)
+            ld.add_filenames({0: [str(p) for p in paths]})
+            fb = ld.copy_files_to_device()
+            ts = [fb.get_tensor(k) for k in ld.get_keys()]
+            torch.cuda.synchronize()
+            del ts
+            fb.close()
+            ld.close()
+
+        t = timed(fst, steps)
+        out["fastsafetensors"] = {"version": getattr(fastsafetensors, "__version__", "0.3.1"), "mode": "nogds",
+                                  "value": round(tensor_bytes / t / 1e9, 3), "unit": "GB/s", "seconds": round(t, 4)}
+    except Exception as e:  # noqa: BLE001 - a baseline that cannot run is reported, not fatal
+        out["fastsafetensors"] = {"error": f"{type(e).__name__}: {e}"[:200]}
+    try:
+        import safetensors
+        from safetensors.torch import load_file
+
+        def st():
+            ts = [load_file(str(p), device=dev) for p in paths]
+            torch.cuda.synchronize()
+            del ts
+
+        t = timed(st, max(1, steps - 1))
+        out["safetensors"] = {"version": safetensors.__version__, "call": "load_file(device=cuda)",
+                              "value": round(tensor_bytes / t / 1e9, 3), "unit": "GB/s", "seconds": round(t, 4)}
+    except Exception as e:  # noqa: BLE001
+        out["safetensors"] = {"error": f"{type(e).__name__}: {e}"[:200]}
+    return out
 
 
 def hbm_peak_gbs() -> tuple[float, str]:
@@ -483,6 +570,7 @@ def main():
     clocks = Clocks(local)
     e2e_ms, launches_e2e, io_modes, h2d_bytes, ring = [], 0, set(), 0, 0.0
     first_ms = None
+    warm_cache(mapping[rank])  # "warm" means resident: O_DIRECT reads of a cold file would not make it so
     for i in range(args.warmup):
         ms, _, _ = e2e_step()
         if first_ms is None:
@@ -515,10 +603,24 @@ def main():
 
     io = None
     cpu = None
+    libs = None
+    views = None
     if rank == 0 and world == 1 and not args.quick:
-        io = io_probes(paths, local)
+        if args.baselines:
+            # apples to apples with upstream (whose get_tensor returns views): our zero-copy mode
+            cfg.auto_release = False
+            warm_cache(paths)  # the cold leg left the files out of the page cache
+            e2e_step()
+            vms = [e2e_step()[0] for _ in range(args.steps)]
+            cfg.auto_release = True
+            views = {"value": round(job_bytes / (statistics.median(vms) / 1e3) / 1e9, 3), "unit": "GB/s",
+                     "seconds_to_ready": round(statistics.median(vms) / 1e3, 4), "auto_release": False}
+            libs = library_baselines(paths, local, tensor_bytes)
         if args.cpu_baseline:
-            cpu = run_cpu_reference(paths, steps=1, warmup=0)
+            if not args.baselines:
+                warm_cache(paths)
+            cpu = run_cpu_reference(paths, steps=1, warmup=0)  # warm page cache, like the e2e leg
+        io = io_probes(paths, local)  # last: it drops the first file from the page cache
 
     if rank == 0:
         roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
@@ -544,6 +646,8 @@ def main():
                     "first_load_seconds_in_process": round(first_ms / 1e3, 4) if first_ms else None,
                     "phases_ms": phase_med},
             "e2e_cold": cold,
+            "e2e_views": views,
+            "library_baselines": libs,
             "roofline": roofline,
             "io_roofline": io,
             "cpu_baseline": cpu,
