@@ -65,27 +65,31 @@ def parse():
                     help="also time upstream fastsafetensors and safetensors on the same files (N=1)")
     ap.add_argument("--files", type=int, default=0,
                     help="re-split the checkpoint into this many files (0: HF split at N=1, N files at N>1)")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="keep only the first N transformer blocks (configs larger than one GPU / the disk)")
+    ap.add_argument("--cast", default=None, help="on-device dtype conversion at retrieval, e.g. F16 (C5)")
     ap.add_argument("--data-plane", default="auto", choices=["auto", "ipc", "nccl"],
                     help="N>1: peer-memory pulls (one hl_gather per rank over NVLink) or NCCL broadcast/scatter")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------------------- data
-def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, dist, files: int | None = None):
+def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, dist, files: int | None = None,
+                layers: int | None = None):
     """Generate the synthetic checkpoint once per box (GPU RNG). ``files``
     re-splits it HF-style into that many roughly equal files (same tensors,
     same order) so that at N ranks every rank owns file bytes to read."""
     from paper_2505_23072_b200 import synth
 
-    ents = synth.entries(arch)
+    ents = synth.entries(arch, layers)
     max_bytes = None
     if files:
         # greedy split: shrink the cap until the file count is reached (or cannot shrink further)
-        cap = -(-synth.total_bytes(arch) // files)
+        cap = -(-sum(synth.nbytes(e) for e in ents) // files)
         while len(synth.split_files(arch, ents, cap)) > files:
             cap = int(cap * 1.02) + 1
         max_bytes = cap
-    tag = f"{arch}-{header}" + (f"-f{files}" if max_bytes else "")
+    tag = f"{arch}-{header}" + (f"-L{layers}" if layers is not None else "") + (f"-f{files}" if max_bytes else "")
     d = Path(data_dir) / tag
     marker = d / "READY"
     if rank == 0 and not marker.exists():
@@ -93,7 +97,7 @@ def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, di
 
         t0 = time.time()
         synth.generate(arch, d, header=header, seed=0, device="cuda" if torch.cuda.is_available() else None,
-                       max_bytes=max_bytes)
+                       max_bytes=max_bytes, layers=layers)
         os.sync()
         marker.write_text(json.dumps({"seconds": time.time() - t0}))
     if world > 1:
@@ -102,10 +106,10 @@ def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, di
     return [d / f"model-{i + 1:05d}-of-{len(groups):05d}.safetensors" for i in range(len(groups))]
 
 
-def synth_split(arch):
+def synth_split(arch, layers=None):
     from paper_2505_23072_b200 import synth
 
-    return synth.split_files(arch)
+    return synth.split_files(arch, synth.entries(arch, layers))
 
 
 def warm_cache(paths, threads: int = 16, chunk: int = 64 << 20) -> None:
@@ -190,14 +194,16 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=None):
+def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=None, cast=None):
     """The reference's CPU load pipeline (oracle port of aggload's loader) on
     the FULL workload of this arm: W thread-ranks (the reference's in-process
     ProcessGroup), files round-robin to ranks, each rank's thread-rule preadv
     workers land its files (transfer.py:197-201, 305-389), then every rank
     retrieves every key — an auto-release clone (loader.py:456-461) or its
     slice along the Megatron dim (collective.py:318-330) — from the owner's
-    host buffer. Returns ready tensor bytes per second over all ranks."""
+    host buffer. ``cast``: the reference's loader cannot convert (SURVEY
+    §8a a7), so its conversion (device.convert_dtype = numpy astype) is applied
+    to each retrieved tensor. Returns ready tensor bytes per second over all ranks."""
     import threading
 
     from oracle import oracle
@@ -221,7 +227,8 @@ def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=Non
             nb = 0
             for k, ld in owner.items():
                 d = policy.get(k) if world > 1 else None
-                nb += (ld.get_tensor(k) if d is None else ld.get_sharded(k, d, world, r)).nbytes
+                tag = cast.value if cast is not None else None
+                nb += (ld.get_tensor(k, tag) if d is None else ld.get_sharded(k, d, world, r, tag)).nbytes
             got[r] = nb
 
         ts = [threading.Thread(target=retrieve, args=(r,)) for r in range(world)]
@@ -240,7 +247,9 @@ def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=Non
             "sample": f"full workload: {len(paths)} file(s), {ready} ready tensor bytes over {world} rank(s), warm "
                       f"page cache; reference thread rule per rank ({sorted(set(workers.values()))} preadv "
                       f"worker(s)), then {world} retrieval thread(s) (auto-release clones"
-                      + (" / Megatron-dim slices" if world > 1 else "") + f"); host os.cpu_count()={os.cpu_count()}"}
+                      + (" / Megatron-dim slices" if world > 1 else "")
+                      + (f", numpy {cast.value} conversion" if cast is not None else "")
+                      + f"); host os.cpu_count()={os.cpu_count()}"}
 
 
 # ----------------------------------------------------------------------------- io probes
@@ -400,25 +409,33 @@ def main():
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n_files = args.files if args.files else (None if world == 1 else max(world, len(synth_split(args.arch))))
-    paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist, n_files)
+    n_files = args.files if args.files else (None if world == 1 else
+                                             max(world, len(synth_split(args.arch, args.layers))))
+    paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist, n_files, args.layers)
     from paper_2505_23072_b200 import synth
 
-    ents = synth.entries(args.arch)
-    tensor_bytes = synth.total_bytes(args.arch)
+    from paper_2505_23072_b200.format import DType
+
+    ents = synth.entries(args.arch, args.layers)
+    tensor_bytes = sum(synth.nbytes(e) for e in ents)
+    cast = DType.from_tag(args.cast.upper()) if args.cast else None
+    src_dt = ents[0][1]
+    dtype_tag = src_dt.value.lower() + (f"->{cast.value.lower()}" if cast else "")
+    workload = (f"{args.arch}{f' (first {args.layers} blocks)' if args.layers is not None else ''} "
+                f"{src_dt.value.lower()} synthetic, {len(paths)} files, "
+                + ("get_tensor every key" if world == 1 else f"TP={world} get_sharded (Megatron dims)")
+                + (f", on-device {src_dt.value}->{cast.value} cast" if cast else ""))
     file_bytes = sum(os.path.getsize(p) for p in paths)
 
     if args.impl == "reference":
         if rank == 0:
             policy = {e[0]: synth.shard_dim(e[0], e[2]) for e in ents}
-            r = run_cpu_reference(paths, args.steps, max(args.warmup, 1), world, policy)
+            r = run_cpu_reference(paths, args.steps, max(args.warmup, 1), world, policy, cast)
             line = {"metric": METRIC, "value": round(r["value"], 4), "unit": "GB/s", "n_gpus": args.gpus,
                     "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["seconds"] * 1e3, 1),
-                    "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                    "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag,
                     "data": "synthetic", "impl": "reference",
-                    "config": {"workload": f"{args.arch} bf16 synthetic, {len(paths)} files, "
-                               + ("get_tensor every key" if world == 1 else f"TP={world} get_sharded (Megatron dims)"),
-                               "global_batch": 1, "seq_len": 0, "parallelism": f"cpu, {world} thread-rank(s)"},
+                    "config": {"workload": workload, "global_batch": 1, "seq_len": 0, "parallelism": f"cpu, {world} thread-rank(s)"},
                     "cpu_baseline": r,
                     "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                             "d2h_bytes_per_step": 0}}
@@ -454,11 +471,12 @@ def main():
         nb = 0
         for name, dt, shape in ents:
             d = policy[name]
+            osz = (cast or dt).size_bytes
             if d is None:
-                nb += math.prod(shape) * dt.size_bytes
+                nb += math.prod(shape) * osz
             else:
                 lo, hi = kernels.shard_bounds(shape[d], world, r)
-                nb += math.prod(shape) // shape[d] * (hi - lo) * dt.size_bytes
+                nb += math.prod(shape) // shape[d] * (hi - lo) * osz
         return nb
 
     job_bytes = sum(ready_bytes_for_rank(r) for r in range(world))
@@ -467,11 +485,11 @@ def main():
 
     def retrieve(fb, batched: bool):
         if batched:
-            return list(fb.get_tensors(keys, dims=dims).values())
+            return list(fb.get_tensors(keys, dtype=cast, dims=dims).values())
         outs = []
         for k in keys:
             d = policy[k]
-            outs.append(fb.get_tensor(k) if d is None else fb.get_sharded(k, d))
+            outs.append(fb.get_tensor(k, dtype=cast) if d is None else fb.get_sharded(k, d, dtype=cast))
         return outs
 
     # ---- value leg: landed bytes in HBM -> ready tensors --------------------------------
@@ -527,7 +545,9 @@ def main():
     tr_file = ROOT / "profiles" / "ncu_traffic.json"
     if tr_file.exists():
         try:
-            traffic = json.loads(tr_file.read_text()).get(f"{args.arch}-{args.header}-w{world}")
+            traffic = json.loads(tr_file.read_text()).get(f"{args.arch}-{args.header}-w{world}"
+                                                                + (f"-L{args.layers}" if args.layers is not None else "")
+                                                                + (f"-{cast.value}" if cast else ""))
         except (OSError, ValueError):
             traffic = None
     landed.close()
@@ -606,7 +626,7 @@ def main():
     libs = None
     views = None
     if rank == 0 and world == 1 and not args.quick:
-        if args.baselines:
+        if args.baselines and cast is None:
             # apples to apples with upstream (whose get_tensor returns views): our zero-copy mode
             cfg.auto_release = False
             warm_cache(paths)  # the cold leg left the files out of the page cache
@@ -619,27 +639,27 @@ def main():
         if args.cpu_baseline:
             if not args.baselines:
                 warm_cache(paths)
-            cpu = run_cpu_reference(paths, steps=1, warmup=0)  # warm page cache, like the e2e leg
+            cpu = run_cpu_reference(paths, steps=1, warmup=0, cast=cast)  # warm page cache, like the e2e leg
         io = io_probes(paths, local)  # last: it drops the first file from the page cache
 
     if rank == 0:
         roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
-                    "traffic": traffic, "kernel": "hl_gather row_kernel<K_COPY1, aligned>",
+                    "traffic": traffic, "kernel": "hl_gather row_kernel<"
+                    + (f"{src_dt.value}->{cast.value}" if cast else "K_COPY1") + ", aligned>",
                     "launches_per_step": k_n, "algorithmic_bytes_per_launch": k_bytes // max(k_n, 1),
                     "peak_source": peak_source}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(value_ms, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.arch} bf16 synthetic, {len(paths)} files, "
-                       + ("get_tensor every key" if world == 1 else f"TP={world} get_sharded (Megatron dims)"),
-                       "tensor_bytes": tensor_bytes, "file_bytes": file_bytes, "ready_bytes_job": job_bytes,
+            "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag, "data": "synthetic",
+            "config": {"workload": workload, "cast": cast.value if cast else None,
+                       "layers": args.layers, "tensor_bytes": tensor_bytes, "file_bytes": file_bytes, "ready_bytes_job": job_bytes,
                        "tensors": len(ents), "header": args.header, "backend": args.backend,
                        "auto_release": True, "global_batch": 1, "seq_len": 0,
                        "parallelism": f"tp{world}" if world > 1 else "single",
                        "data_plane": group.data_plane if world > 1 else None,
-                       "l2": "inputs (13.5 GB) far exceed the 126 MB L2; no flush needed"},
+                       "l2": f"inputs ({tensor_bytes / 1e9:.1f} GB) far exceed the 126 MB L2; no flush needed"},
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "seconds_to_ready": round(e2e_med / 1e3, 4),
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h, "page_cache": "warm",
                     "io_modes": sorted(io_modes), "ring_setup_seconds_first_load": round(ring, 4),
