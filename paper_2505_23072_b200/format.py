@@ -68,19 +68,14 @@ class DType(Enum):
     F32 = "F32"
     F64 = "F64"
 
-    @property
-    def size_bytes(self) -> int:
-        return _SIZES[self.value]
-
-    @property
-    def alignment(self) -> int:
-        # element-access alignment == element size (ref format.py:67-71)
-        return _SIZES[self.value]
-
-    @property
-    def code(self) -> int:
-        """Numeric tag used in device descriptors (include/hbmload.h HL_DT_*)."""
-        return _CODES[self.value]
+    # size_bytes / alignment (element-access alignment == element size, ref
+    # format.py:67-71) / code (numeric tag of device descriptors,
+    # include/hbmload.h HL_DT_*) are plain member attributes set below: the
+    # retrieval hot path reads them per key, and an Enum property costs ~10x
+    # an attribute load.
+    size_bytes: int
+    alignment: int
+    code: int
 
     @classmethod
     def from_tag(cls, tag: str) -> "DType":
@@ -94,6 +89,10 @@ _SIZES = {"BOOL": 1, "U8": 1, "I8": 1, "I16": 2, "U16": 2, "I32": 4, "U32": 4,
           "I64": 8, "U64": 8, "F16": 2, "BF16": 2, "F32": 4, "F64": 8}
 _CODES = {tag: i for i, tag in enumerate(
     ["BOOL", "U8", "I8", "I16", "U16", "I32", "U32", "I64", "U64", "F16", "BF16", "F32", "F64"])}
+for _m in DType:
+    _m.size_bytes = _m.alignment = _SIZES[_m.value]
+    _m.code = _CODES[_m.value]
+del _m
 
 
 def numel(shape: Iterable[int]) -> int:

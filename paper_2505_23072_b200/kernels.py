@@ -61,18 +61,26 @@ def algorithmic_bytes(descs: list[Desc]) -> int:
     return sum(d[2] * d[3] * (_SIZE[d[5]] + _SIZE[d[6]]) for d in descs)
 
 
+try:  # the raw cudaStream_t of the device's current stream, without building a Stream object
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover
+    def _raw_stream(index: int) -> int:
+        return torch.cuda.current_stream(index).cuda_stream
+
+
 def run(descs: list[Desc], device: torch.device) -> None:
-    """Enqueue the batch on ``device``'s current stream (the launch goes to the
-    stream's device; hl_gather switches to it when the caller's differs)."""
+    """Enqueue the batch on ``device``'s current stream. hl_gather launches on
+    the CURRENT device (grid sizing and the launch itself), so switch to the
+    stream's device when the caller's differs."""
     if not descs:
         return
     if torch.cuda.current_device() != device.index:
         with torch.cuda.device(device):
             return run(descs, device)
-    stream = torch.cuda.current_stream(device)
     if TIMING is None:
-        _native.gather(descs, stream.cuda_stream)
+        _native.gather(descs, _raw_stream(device.index))
         return
+    stream = torch.cuda.current_stream(device)
     table, n = _native.pack(descs)  # host-side table build stays outside the timed launch
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
