@@ -37,7 +37,11 @@ struct Mapping {
 };
 std::mutex g_mu;
 std::map<std::string, Mapping> g_by_handle;        // handle bytes -> mapping
-std::map<uintptr_t, std::string> g_handle_of_ptr;  // returned pointer -> handle key
+struct Imported {
+  std::string key;  // handle bytes of the mapping the pointer lies in
+  int count = 0;    // imports of this exact pointer not yet released
+};
+std::map<uintptr_t, Imported> g_handle_of_ptr;  // returned pointer -> mapping
 }  // namespace
 
 extern "C" int hl_ipc_export(const void* dev_ptr, hl_ipc_handle* out) {
@@ -65,10 +69,13 @@ extern "C" int hl_ipc_import(const hl_ipc_handle* hd, int device, void** out_ptr
   std::lock_guard<std::mutex> g(g_mu);
   Mapping& m = g_by_handle[key];
   if (!m.base) {
-    cudaSetDevice(device);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);  // the mapping belongs to the importing device's context
     cudaIpcMemHandle_t h;
     memcpy(&h, hd->handle, 64);
     cudaError_t e = cudaIpcOpenMemHandle(&m.base, h, cudaIpcMemLazyEnablePeerAccess);
+    cudaSetDevice(prev);
     if (e != cudaSuccess) {
       g_by_handle.erase(key);
       return set_error(HL_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
@@ -76,7 +83,9 @@ extern "C" int hl_ipc_import(const hl_ipc_handle* hd, int device, void** out_ptr
   }
   m.refs++;
   void* p = (uint8_t*)m.base + hd->offset;
-  g_handle_of_ptr[(uintptr_t)p] = key;
+  Imported& imp = g_handle_of_ptr[(uintptr_t)p];
+  imp.key = key;
+  imp.count++;
   *out_ptr = p;
   return HL_OK;
 }
@@ -86,12 +95,12 @@ extern "C" int hl_ipc_release(void* ptr) {
   std::lock_guard<std::mutex> g(g_mu);
   auto it = g_handle_of_ptr.find((uintptr_t)ptr);
   if (it == g_handle_of_ptr.end()) return set_error(HL_EINVAL, "pointer %p was not imported", ptr);
-  auto mt = g_by_handle.find(it->second);
+  auto mt = g_by_handle.find(it->second.key);
   if (mt != g_by_handle.end() && --mt->second.refs <= 0) {
     cudaIpcCloseMemHandle(mt->second.base);
     g_by_handle.erase(mt);
   }
-  g_handle_of_ptr.erase(it);
+  if (--it->second.count <= 0) g_handle_of_ptr.erase(it);
   return HL_OK;
 }
 
