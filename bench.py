@@ -409,8 +409,9 @@ def main():
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n_files = args.files if args.files else (None if world == 1 else
-                                             max(world, len(synth_split(args.arch, args.layers))))
+    # at N ranks every rank must own file bytes: re-split only when the HF split has fewer than N files
+    hf_files = len(synth_split(args.arch, args.layers))
+    n_files = args.files if args.files else (None if world <= hf_files else world)
     paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist, n_files, args.layers)
     from paper_2505_23072_b200 import synth
 
@@ -467,11 +468,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def ready_bytes_for_rank(r: int) -> int:
+    def ready_bytes_for_rank(r: int, out: bool = False) -> int:
+        """Tensor body bytes rank r makes ready (its slices of sharded keys);
+        out=True counts them in the retrieval dtype instead."""
         nb = 0
         for name, dt, shape in ents:
             d = policy[name]
-            osz = (cast or dt).size_bytes
+            osz = (cast or dt).size_bytes if out else dt.size_bytes
             if d is None:
                 nb += math.prod(shape) * osz
             else:
@@ -479,7 +482,8 @@ def main():
                 nb += math.prod(shape) // shape[d] * (hi - lo) * osz
         return nb
 
-    job_bytes = sum(ready_bytes_for_rank(r) for r in range(world))
+    job_bytes = sum(ready_bytes_for_rank(r) for r in range(world))  # the metric: Σ tensor body bytes
+    out_bytes = sum(ready_bytes_for_rank(r, out=True) for r in range(world))
 
     dims = {k: d for k, d in policy.items() if d is not None}
 
@@ -654,7 +658,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(value_ms, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag, "data": "synthetic",
             "config": {"workload": workload, "cast": cast.value if cast else None,
-                       "layers": args.layers, "tensor_bytes": tensor_bytes, "file_bytes": file_bytes, "ready_bytes_job": job_bytes,
+                       "layers": args.layers, "tensor_bytes": tensor_bytes, "file_bytes": file_bytes, "ready_bytes_job": job_bytes, "ready_bytes_out": out_bytes,
                        "tensors": len(ents), "header": args.header, "backend": args.backend,
                        "auto_release": True, "global_batch": 1, "seq_len": 0,
                        "parallelism": f"tp{world}" if world > 1 else "single",

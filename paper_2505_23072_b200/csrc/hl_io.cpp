@@ -573,9 +573,11 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     uint32_t mode = ctx->cfg.io_mode;
     // cuFile only where it is real GPUDirect Storage (nvidia-fs loaded); without
     // it cuFile's compat mode is a slower POSIX bounce path than our own ring,
-    // so the GDS-shaped backend reads with O_DIRECT instead (HL_FORCE_CUFILE=1
-    // keeps cuFile for experiments).
-    if (mode == HL_IO_CUFILE && !hl_gds_available() && !getenv("HL_FORCE_CUFILE")) mode = HL_IO_DIRECT;
+    // so the GDS-shaped backend reads through the ring instead: O_DIRECT for
+    // what is on storage, the page cache for what is already resident (AUTO's
+    // per-chunk probe; a warm file would otherwise be re-read from the disk).
+    // HL_FORCE_CUFILE=1 keeps cuFile for experiments.
+    if (mode == HL_IO_CUFILE && !hl_gds_available() && !getenv("HL_FORCE_CUFILE")) mode = HL_IO_AUTO;
     if (mode == HL_IO_AUTO && f.size) {
       void* m = mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0);
       if (m != MAP_FAILED) f.probe = (uint8_t*)m;
