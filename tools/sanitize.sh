@@ -1,0 +1,18 @@
+#!/bin/bash
+# compute-sanitizer over hl_gather (race detection / memory checking on the kernel).
+# memcheck + initcheck on the kernel and loader tests (the 48 MiB cases excluded: sanitizer replay
+# is ~100x slower), racecheck on the kernel tests (the kernel uses warp shuffles, no shared memory).
+mkdir -p gpurun_out
+CS=/usr/local/cuda/bin/compute-sanitizer
+K='--kernel-name regex:row_kernel --kernel-name regex:generic_kernel'
+T=${T:-1500}
+for tool in memcheck initcheck racecheck; do
+  files="tests/test_kernel_gpu.py"
+  [ $tool != racecheck ] && files="$files tests/test_loader_gpu.py tests/test_golden_gpu.py"
+  timeout $T $CS --tool $tool $K --error-exitcode 99 --print-limit 20 --log-file gpurun_out/sanitize_$tool.txt \
+      python -m pytest $files -m gpu -q -p no:cacheprovider -k "not large" \
+      > gpurun_out/sanitize_${tool}_pytest.log 2>&1
+  echo "$tool exit $?" | tee -a gpurun_out/sanitize_summary.txt
+  tail -3 gpurun_out/sanitize_$tool.txt >> gpurun_out/sanitize_summary.txt
+  tail -1 gpurun_out/sanitize_${tool}_pytest.log >> gpurun_out/sanitize_summary.txt
+done
