@@ -4,7 +4,7 @@
 # is ~100x slower), racecheck on the kernel tests (the kernel uses warp shuffles, no shared memory).
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
-K='--kernel-name regex:row_kernel --kernel-name regex:generic_kernel'
+K='--kernel-name kns=row_kernel --kernel-name kns=generic_kernel'
 T=${T:-1500}
 for tool in memcheck initcheck racecheck; do
   files="tests/test_kernel_gpu.py"

@@ -1,0 +1,166 @@
+// storage_probe.c — how fast can this box's storage deliver a cold file?
+// O_DIRECT reads, (a) T threads of synchronous pread, (b) one io_uring ring at
+// queue depth Q (raw syscalls, no liburing). Prints one JSON line per config.
+//   gcc -O2 -pthread -o /tmp/storage_probe tools/storage_probe.c
+//   /tmp/storage_probe FILE      (drops the file from the page cache before each run)
+#define _GNU_SOURCE
+#include <fcntl.h>
+#include <linux/io_uring.h>
+#include <pthread.h>
+#include <stdatomic.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <sys/syscall.h>
+#include <time.h>
+#include <unistd.h>
+
+static const char* g_path;
+static uint64_t g_size, g_chunk;
+static atomic_uint_fast64_t g_cursor;
+
+static double now(void) {
+  struct timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return t.tv_sec + t.tv_nsec * 1e-9;
+}
+
+static void drop(void) {
+  int fd = open(g_path, O_RDONLY);
+  fdatasync(fd);
+  posix_fadvise(fd, 0, 0, POSIX_FADV_DONTNEED);
+  close(fd);
+}
+
+static void* worker(void* arg) {
+  (void)arg;
+  int fd = open(g_path, O_RDONLY | O_DIRECT);
+  void* buf;
+  if (posix_memalign(&buf, 4096, g_chunk)) return NULL;
+  for (;;) {
+    uint64_t off = atomic_fetch_add(&g_cursor, g_chunk);
+    if (off >= g_size) break;
+    uint64_t n = g_size - off < g_chunk ? g_size - off : g_chunk;
+    n = (n + 4095) & ~4095ull;
+    if (pread(fd, buf, n, off) < 0) break;
+  }
+  free(buf);
+  close(fd);
+  return NULL;
+}
+
+static void threads(int t, uint64_t chunk) {
+  drop();
+  g_chunk = chunk;
+  atomic_store(&g_cursor, 0);
+  pthread_t th[256];
+  double t0 = now();
+  for (int i = 0; i < t; ++i) pthread_create(&th[i], NULL, worker, NULL);
+  for (int i = 0; i < t; ++i) pthread_join(th[i], NULL);
+  double dt = now() - t0;
+  printf("{\"probe\": \"pread_threads\", \"threads\": %d, \"chunk_mb\": %.2f, \"GBps\": %.3f}\n", t,
+         chunk / 1048576.0, g_size / dt / 1e9);
+  fflush(stdout);
+}
+
+static int uring_setup(unsigned entries, struct io_uring_params* p) {
+  return (int)syscall(__NR_io_uring_setup, entries, p);
+}
+static int uring_enter(int fd, unsigned submit, unsigned wait, unsigned flags) {
+  return (int)syscall(__NR_io_uring_enter, fd, submit, wait, flags, NULL, 0);
+}
+
+static void uring(unsigned qd, uint64_t chunk) {
+  drop();
+  struct io_uring_params p;
+  memset(&p, 0, sizeof p);
+  int rfd = uring_setup(qd, &p);
+  if (rfd < 0) {
+    printf("{\"probe\": \"io_uring\", \"error\": \"io_uring_setup failed (%s)\"}\n", strerror(-rfd > 0 ? -rfd : 1));
+    fflush(stdout);
+    return;
+  }
+  size_t sq_sz = p.sq_off.array + p.sq_entries * sizeof(unsigned);
+  size_t cq_sz = p.cq_off.cqes + p.cq_entries * sizeof(struct io_uring_cqe);
+  uint8_t* sq = mmap(NULL, sq_sz, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rfd, IORING_OFF_SQ_RING);
+  uint8_t* cq = mmap(NULL, cq_sz, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, rfd, IORING_OFF_CQ_RING);
+  struct io_uring_sqe* sqes = mmap(NULL, p.sq_entries * sizeof(struct io_uring_sqe), PROT_READ | PROT_WRITE,
+                                   MAP_SHARED | MAP_POPULATE, rfd, IORING_OFF_SQES);
+  unsigned* sq_tail = (unsigned*)(sq + p.sq_off.tail);
+  unsigned* sq_mask = (unsigned*)(sq + p.sq_off.ring_mask);
+  unsigned* sq_array = (unsigned*)(sq + p.sq_off.array);
+  unsigned* cq_head = (unsigned*)(cq + p.cq_off.head);
+  unsigned* cq_tail = (unsigned*)(cq + p.cq_off.tail);
+  unsigned* cq_mask = (unsigned*)(cq + p.cq_off.ring_mask);
+  struct io_uring_cqe* cqes = (struct io_uring_cqe*)(cq + p.cq_off.cqes);
+  int fd = open(g_path, O_RDONLY | O_DIRECT);
+  uint8_t* bufs;
+  if (posix_memalign((void**)&bufs, 4096, (size_t)qd * chunk)) return;
+  uint64_t next = 0, done = 0;
+  unsigned inflight = 0;
+  double t0 = now();
+  unsigned free_slots[1024];
+  unsigned nfree = qd;
+  for (unsigned i = 0; i < qd; ++i) free_slots[i] = i;
+  while (done < g_size) {
+    unsigned queued = 0;
+    while (nfree && next < g_size) {
+      unsigned slot = free_slots[--nfree];
+      unsigned tail = *sq_tail;
+      unsigned idx = tail & *sq_mask;
+      struct io_uring_sqe* e = &sqes[idx];
+      memset(e, 0, sizeof *e);
+      uint64_t n = g_size - next < chunk ? g_size - next : chunk;
+      e->opcode = IORING_OP_READ;
+      e->fd = fd;
+      e->addr = (uint64_t)(uintptr_t)(bufs + (size_t)slot * chunk);
+      e->len = (uint32_t)((n + 4095) & ~4095ull);
+      e->off = next;
+      e->user_data = ((uint64_t)slot << 40) | n;
+      sq_array[idx] = idx;
+      __atomic_store_n(sq_tail, tail + 1, __ATOMIC_RELEASE);
+      next += n;
+      ++queued;
+      ++inflight;
+    }
+    int r = uring_enter(rfd, queued, 1, IORING_ENTER_GETEVENTS);
+    if (r < 0) break;
+    unsigned head = *cq_head;
+    while (head != __atomic_load_n(cq_tail, __ATOMIC_ACQUIRE)) {
+      struct io_uring_cqe* c = &cqes[head & *cq_mask];
+      if (c->res < 0) { printf("{\"probe\": \"io_uring\", \"error\": \"read failed %d\"}\n", c->res); return; }
+      done += c->user_data & ((1ull << 40) - 1);
+      free_slots[nfree++] = (unsigned)(c->user_data >> 40);
+      --inflight;
+      ++head;
+    }
+    __atomic_store_n(cq_head, head, __ATOMIC_RELEASE);
+  }
+  double dt = now() - t0;
+  printf("{\"probe\": \"io_uring\", \"qd\": %u, \"chunk_mb\": %.2f, \"GBps\": %.3f}\n", qd, chunk / 1048576.0,
+         g_size / dt / 1e9);
+  fflush(stdout);
+  close(fd);
+  close(rfd);
+  free(bufs);
+}
+
+int main(int argc, char** argv) {
+  if (argc < 2) return 2;
+  g_path = argv[1];
+  struct stat st;
+  if (stat(g_path, &st)) return 2;
+  g_size = (uint64_t)st.st_size & ~4095ull;
+  threads(16, 16 << 20);
+  threads(32, 4 << 20);
+  threads(64, 1 << 20);
+  threads(64, 4 << 20);
+  uring(32, 1 << 20);
+  uring(64, 1 << 20);
+  uring(128, 512 << 10);
+  uring(64, 4 << 20);
+  return 0;
+}
