@@ -30,10 +30,8 @@
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
-#include <sys/syscall.h>
 #include <sys/uio.h>
 #include <unistd.h>
-#include <linux/io_uring.h>
 
 #include <algorithm>
 #include <atomic>
@@ -151,148 +149,10 @@ struct Slot {
   bool busy = false;
   void* reg = nullptr;  // HL_IO_MMAP: page-cache range pinned for the in-flight DMA
 };
-// Per-worker io_uring for the O_DIRECT part of a chunk: the chunk is cut into
-// kUringPiece reads submitted together, so each worker keeps several requests
-// in flight (measured on the B200 box's virtio disk, cold: one ring at depth
-// 32 x 1 MiB reads 5.5 GB/s, 16-64 threads of synchronous pread 4.6-4.7 GB/s;
-// profiles/r01_storage_probe.jsonl). Raw syscalls, no liburing. Where the
-// kernel or a seccomp profile refuses io_uring the worker keeps using pread.
-static constexpr uint64_t kUringPiece = 1ull << 20;
-static constexpr unsigned kUringDepth = 32;
-
-struct Uring {
-  int fd = -1;
-  bool tried = false;
-  unsigned *sq_tail = nullptr, *sq_mask = nullptr, *sq_array = nullptr;
-  unsigned *cq_head = nullptr, *cq_tail = nullptr, *cq_mask = nullptr;
-  io_uring_sqe* sqes = nullptr;
-  io_uring_cqe* cqes = nullptr;
-  void* sq_map = nullptr;
-  void* cq_map = nullptr;
-  size_t sq_len = 0, cq_len = 0, sqe_len = 0;
-
-  bool ready() {
-    if (tried) return fd >= 0;
-    tried = true;
-    if (getenv("HL_NO_IO_URING")) return false;
-    io_uring_params p;
-    memset(&p, 0, sizeof p);
-    int r = (int)syscall(__NR_io_uring_setup, kUringDepth, &p);
-    if (r < 0) return false;
-    fd = r;
-    sq_len = p.sq_off.array + p.sq_entries * sizeof(unsigned);
-    cq_len = p.cq_off.cqes + p.cq_entries * sizeof(io_uring_cqe);
-    sqe_len = p.sq_entries * sizeof(io_uring_sqe);
-    sq_map = mmap(nullptr, sq_len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, IORING_OFF_SQ_RING);
-    cq_map = mmap(nullptr, cq_len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, IORING_OFF_CQ_RING);
-    void* e = mmap(nullptr, sqe_len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, IORING_OFF_SQES);
-    if (sq_map == MAP_FAILED || cq_map == MAP_FAILED || e == MAP_FAILED) {
-      close_ring();
-      return false;
-    }
-    uint8_t* sq = (uint8_t*)sq_map;
-    uint8_t* cq = (uint8_t*)cq_map;
-    sq_tail = (unsigned*)(sq + p.sq_off.tail);
-    sq_mask = (unsigned*)(sq + p.sq_off.ring_mask);
-    sq_array = (unsigned*)(sq + p.sq_off.array);
-    cq_head = (unsigned*)(cq + p.cq_off.head);
-    cq_tail = (unsigned*)(cq + p.cq_off.tail);
-    cq_mask = (unsigned*)(cq + p.cq_off.ring_mask);
-    cqes = (io_uring_cqe*)(cq + p.cq_off.cqes);
-    sqes = (io_uring_sqe*)e;
-    return true;
-  }
-
-  void close_ring() {
-    if (sqes && sqes != MAP_FAILED) munmap(sqes, sqe_len);
-    if (sq_map && sq_map != MAP_FAILED) munmap(sq_map, sq_len);
-    if (cq_map && cq_map != MAP_FAILED) munmap(cq_map, cq_len);
-    if (fd >= 0) ::close(fd);
-    fd = -1;
-    sqes = nullptr;
-    sq_map = cq_map = nullptr;
-  }
-
-  // Read [off, off+len) of `dfd` into `dst` (all 4 KiB aligned) as kUringPiece
-  // requests in flight together. *got = bytes valid from the start (a short
-  // piece = EOF). Returns false with *err = errno on a failed request.
-  bool read(int dfd, uint8_t* dst, uint64_t len, uint64_t off, uint64_t* got, int* err) {
-    const uint64_t pieces = (len + kUringPiece - 1) / kUringPiece;
-    std::vector<int64_t> res(pieces, -1);
-    uint64_t next = 0, done = 0;
-    *err = 0;
-    while (done < pieces) {
-      unsigned queued = 0;
-      while (next < pieces && next - done < kUringDepth) {
-        const unsigned tail = *sq_tail;
-        const unsigned idx = tail & *sq_mask;
-        io_uring_sqe* e = &sqes[idx];
-        memset(e, 0, sizeof *e);
-        const uint64_t po = next * kUringPiece;
-        e->opcode = IORING_OP_READ;
-        e->fd = dfd;
-        e->addr = (uint64_t)(uintptr_t)(dst + po);
-        e->len = (uint32_t)std::min<uint64_t>(kUringPiece, len - po);
-        e->off = off + po;
-        e->user_data = next;
-        sq_array[idx] = idx;
-        __atomic_store_n(sq_tail, tail + 1, __ATOMIC_RELEASE);
-        ++next;
-        ++queued;
-      }
-      int r;
-      do {  // a retry re-offers `queued`: the kernel only submits entries it has not consumed yet
-        r = (int)syscall(__NR_io_uring_enter, fd, queued, 1, IORING_ENTER_GETEVENTS, nullptr, 0);
-      } while (r < 0 && errno == EINTR);
-      if (r < 0) {
-        *err = errno;
-        close_ring();  // tearing the ring down waits out its in-flight reads; later chunks use pread
-        return false;  // the caller re-reads this range with pread
-      }
-      unsigned head = *cq_head;
-      while (head != __atomic_load_n(cq_tail, __ATOMIC_ACQUIRE)) {
-        const io_uring_cqe* c = &cqes[head & *cq_mask];
-        res[c->user_data] = c->res;
-        ++done;
-        ++head;
-      }
-      __atomic_store_n(cq_head, head, __ATOMIC_RELEASE);
-    }
-    uint64_t total = 0;
-    for (uint64_t i = 0; i < pieces; ++i) {
-      if (res[i] < 0) {
-        *err = (int)-res[i];
-        *got = total;
-        return false;
-      }
-      const uint64_t want = std::min<uint64_t>(kUringPiece, len - i * kUringPiece);
-      if ((uint64_t)res[i] < want) {  // short piece: a partial request is retried with pread, EOF stops
-        uint64_t more = 0;
-        int e2 = 0;
-        const uint64_t po = i * kUringPiece + (uint64_t)res[i];
-        if (!pread_tail(dfd, dst + po, want - (uint64_t)res[i], off + po, &more, &e2)) {
-          *err = e2;
-          *got = total + (uint64_t)res[i];
-          return false;
-        }
-        total += (uint64_t)res[i] + more;
-        if ((uint64_t)res[i] + more < want) break;  // EOF
-        continue;
-      }
-      total += want;
-    }
-    *got = total;
-    return true;
-  }
-
-  static bool pread_tail(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got, int* err);
-};
-
 struct WorkerRing {
   std::vector<Slot> slots;
   cudaStream_t stream = nullptr;
   size_t next = 0;
-  Uring uring;
 };
 
 struct hl_ctx {
@@ -361,14 +221,6 @@ bool pread_full(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got,
   *err = 0;
   return true;
 }
-
-}  // namespace
-
-bool Uring::pread_tail(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got, int* err) {
-  return pread_full(fd, buf, len, off, got, err);
-}
-
-namespace {
 
 // Stream + event per slot now; the pinned memory of a slot is allocated the
 // first time the slot is used, so a fresh process starts reading into slot 0
@@ -527,15 +379,7 @@ void worker_main(PlanRun* run, uint32_t w) {
         uint8_t* dst = s.host + (aoff - (c.off - head));  // 4 KiB aligned: aoff >= c.off - head
         uint64_t got = 0;
         int err = 0;
-        bool ok = false;
-        if (f.dfd >= 0 && ring.uring.ready()) {
-          ok = ring.uring.read(f.dfd, dst, alen, aoff, &got, &err);
-          if (!ok && err != EINVAL && err != EIO && err != 0) {  // ring refused (not the file): pread it
-            ok = pread_full(f.dfd, dst, alen, aoff, &got, &err);
-          }
-        } else if (f.dfd >= 0) {
-          ok = pread_full(f.dfd, dst, alen, aoff, &got, &err);
-        }
+        bool ok = f.dfd >= 0 && pread_full(f.dfd, dst, alen, aoff, &got, &err);
         if (ok && aoff + got < c.off + c.len) {
           run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(aoff + got));
           return;
@@ -653,7 +497,6 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
       if (s.host) cudaFreeHost(s.host);
     }
     if (r.stream) cudaStreamDestroy(r.stream);
-    r.uring.close_ring();
   }
   delete ctx;
   return HL_OK;
