@@ -726,6 +726,10 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     if (mode == HL_IO_AUTO && f.size) {
       void* m = mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0);
       if (m != MAP_FAILED) f.probe = (uint8_t*)m;
+      // AUTO copies only pages mincore found resident; kernel readahead on those
+      // preads would pull the next (cold) chunks into the cache ahead of their
+      // probes and turn the whole cold remainder into buffered reads
+      posix_fadvise(f.bfd, 0, 0, POSIX_FADV_RANDOM);
     }
     if (mode == HL_IO_MMAP) {
       void* m = f.size ? mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0) : MAP_FAILED;

@@ -104,12 +104,21 @@ def test_forced_cufile_compat_mode_in_subprocess(blob, tmp_path):
 
 
 def test_auto_mode_is_per_chunk_hybrid(blob):
-    """AUTO reads what the page cache holds (RWF_NOWAIT probe) and the rest with
+    """AUTO reads what the page cache holds (mincore probe) and the rest with
     O_DIRECT, per chunk: a half-cached file uses both paths and lands exactly."""
+    import os
+    import time
+
     path, data = blob
     _native.drop_cache(str(path))
-    with open(path, "rb") as f:  # warm the first half only
-        f.read(data.size // 2)
+    # warm the first half only, with WILLNEED: a read() would leave readahead
+    # markers whose async readahead pulls the cold half in ahead of the probes
+    fd = os.open(str(path), os.O_RDONLY)
+    os.posix_fadvise(fd, 0, data.size // 2, os.POSIX_FADV_WILLNEED)
+    os.close(fd)
+    t0 = time.time()
+    while _native.file_residency(str(path)) < 0.45 and time.time() - t0 < 5:
+        time.sleep(0.05)
     eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode="auto")
     dst = torch.zeros(data.size, dtype=torch.uint8, device="cuda")
     st = eng.execute([str(path)], [(0, 0, 0, data.size, dst.data_ptr())])
