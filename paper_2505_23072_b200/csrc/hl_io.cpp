@@ -400,6 +400,7 @@ bool batched_chunk(PlanRun* run, WorkerRing& ring, const Chunk& c, std::vector<u
         }
         bs.batch = c.batch;
         bs.pending = bt.count;
+        ctx->bcv.notify_all();  // the batch's other chunks (and the next batch's waiters) may go on
         break;
       }
       const double tw = now_s();
