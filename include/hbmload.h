@@ -89,8 +89,7 @@ typedef struct hl_config {
   uint32_t slots_per_worker; /* pinned ring depth per worker (0 = 3)                       */
   uint32_t io_mode;          /* enum hl_io_mode                                            */
   int32_t numa_node;         /* pin workers + ring to this node; -1 = the GPU's node       */
-  uint32_t dma_chunks;       /* consecutive chunks coalesced into one H2D copy (0 = ~32 MiB
-                                worth; 1 = one copy per chunk); env HL_DMA_CHUNKS overrides */
+  uint32_t reserved;
 } hl_config;
 
 /* One transfer block: file bytes [file_off, file_off+len) -> device address dev_dst.

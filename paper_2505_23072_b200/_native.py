@@ -36,7 +36,7 @@ class hl_config(C.Structure):
         ("slots_per_worker", C.c_uint32),
         ("io_mode", C.c_uint32),
         ("numa_node", C.c_int32),
-        ("dma_chunks", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -174,16 +174,16 @@ class IoEngine:
     """One hl_ctx: worker threads' pinned ring + streams for one device."""
 
     def __init__(self, device: int, workers: int = 0, chunk_bytes: int = 0,
-                 slots_per_worker: int = 0, io_mode: str = "auto", numa_node: int = -1, dma_chunks: int = 0):
+                 slots_per_worker: int = 0, io_mode: str = "auto", numa_node: int = -1):
         lib = load()
-        cfg = hl_config(device, workers, chunk_bytes, slots_per_worker, IO_MODES[io_mode], numa_node, dma_chunks)
+        cfg = hl_config(device, workers, chunk_bytes, slots_per_worker, IO_MODES[io_mode], numa_node, 0)
         h = C.c_void_p()
         check(lib.hl_ctx_create(C.byref(cfg), C.byref(h)))
         self._h = h
         self._lib = lib
         eff = hl_config()
         check(lib.hl_ctx_config(h, C.byref(eff)))
-        self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_}
+        self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_ if f != "reserved"}
 
     def execute(self, paths: list[str], blocks: list[tuple[int, int, int, int, int]]) -> dict:
         """blocks: (file_index, worker_hint, file_off, len, dev_dst). Blocking."""

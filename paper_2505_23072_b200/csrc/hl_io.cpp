@@ -21,14 +21,6 @@
 // The ring is allocated once per context (lazily, inside the workers so the
 // pages are first-touched on the workers' NUMA node) and reused by every
 // later plan; its cost is reported in hl_plan_stats.ring_setup_seconds.
-//
-// DMA batching (buffered / O_DIRECT / auto reads): pinned H2D throughput
-// depends on the copy size (B200 box, PCIe Gen5 x16: 4 MiB copies 52.8 GB/s,
-// 16 MiB 54.8, 64 MiB 55.4; profiles/r01_h2d_probe.jsonl) while the page-cache
-// pread is fastest at 4 MiB per call. So reads stay chunk-sized but land in a
-// shared ring of batch slots: up to `dma_chunks` consecutive chunks of one
-// contiguous range share a slot, are read by whichever workers claim them, and
-// the worker that completes a batch issues ONE cudaMemcpyAsync for all of it.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdlib.h>
@@ -44,7 +36,6 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
-#include <condition_variable>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -164,26 +155,12 @@ struct WorkerRing {
   size_t next = 0;
 };
 
-// One slot of the shared batch ring: holds batch `batch` (slot s hosts batches
-// s, s+B, s+2B, ... in order) while `pending` of its chunks are being read.
-struct BatchSlot {
-  uint8_t* host = nullptr;
-  cudaEvent_t ev = nullptr;
-  int64_t batch = 0;
-  uint32_t pending = 0;
-  bool dma = false;  // the batch's copy was issued and `ev` recorded after it
-};
-
 struct hl_ctx {
   hl_config cfg{};
   std::vector<int> cpus;
   std::vector<WorkerRing> rings;
   bool ring_ready = false;
   uint64_t slot_bytes = 0;
-  std::vector<BatchSlot> bslots;
-  uint64_t bslot_bytes = 0;
-  std::mutex bmu;
-  std::condition_variable bcv;
   std::mutex mu;  // one plan at a time per context
 };
 
@@ -192,15 +169,6 @@ namespace {
 struct Chunk {
   uint32_t file;
   uint64_t off, len, dst;
-  int64_t batch = -1;  // index into PlanRun::batches, -1 = per-chunk copy (mmap / cuFile)
-};
-
-struct Batch {
-  uint64_t base;   // file offset at slot byte 0 (4 KiB aligned)
-  uint64_t off;    // first file byte of the batch
-  uint64_t len;    // bytes, contiguous in the file and on the device
-  uint64_t dst;    // device address of `off`
-  uint32_t count;  // chunks
 };
 
 struct FileState {
@@ -215,7 +183,6 @@ struct FileState {
 struct PlanRun {
   hl_ctx* ctx;
   const std::vector<Chunk>* chunks;
-  const std::vector<Batch>* batches;
   std::vector<FileState>* files;
   std::atomic<size_t> cursor{0};
   std::atomic<bool> failed{false};
@@ -228,16 +195,12 @@ struct PlanRun {
   std::atomic<uint64_t> read_ns{0}, wait_ns{0}, submit_ns{0};
 
   void fail(int code, const std::string& msg) {
-    {
-      std::lock_guard<std::mutex> g(err_mu);
-      if (err_code == HL_OK) {
-        err_code = code;
-        err_msg = msg;
-      }
-      failed.store(true);
+    std::lock_guard<std::mutex> g(err_mu);
+    if (err_code == HL_OK) {
+      err_code = code;
+      err_msg = msg;
     }
-    std::lock_guard<std::mutex> g(ctx->bmu);  // wake workers waiting for a batch slot
-    ctx->bcv.notify_all();
+    failed.store(true);
   }
 };
 
@@ -285,156 +248,6 @@ int ensure_slot(hl_ctx* ctx, Slot& s) {
   return HL_OK;
 }
 
-// Read chunk `c` (buffered, O_DIRECT or the auto hybrid) into pinned memory
-// `base`, where slot byte 0 corresponds to file offset `base_off` (4 KiB
-// aligned, <= c.off). The O_DIRECT part lands 4 KiB aligned because `base` is.
-bool read_chunk(PlanRun* run, FileState& f, const Chunk& c, uint8_t* base, uint64_t base_off,
-                std::vector<unsigned char>& vec) {
-  uint8_t* at = base + (c.off - base_off);  // where c.off lands
-  uint64_t cached = 0;                       // leading bytes served from the page cache
-  if (f.mode == HL_IO_BUFFERED || (f.mode == HL_IO_DIRECT && f.dfd < 0)) {
-    uint64_t got = 0;
-    int err = 0;
-    if (!pread_full(f.bfd, at, c.len, c.off, &got, &err)) {
-      run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err));
-      return false;
-    }
-    if (got < c.len) {
-      run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(c.off + got) + " (" +
-                            std::to_string(c.len - got) + " bytes short)");
-      return false;
-    }
-    cached = c.len;
-  } else {
-    if (f.mode == HL_IO_AUTO && f.probe) {
-      // hybrid: the page-cache-resident prefix of the chunk (mincore: no I/O is
-      // triggered, unlike a RWF_NOWAIT probe whose readahead would race the
-      // O_DIRECT reads) is copied from the cache, the rest read with O_DIRECT
-      const uint64_t p0 = c.off / kAlign, p1 = (c.off + c.len + kAlign - 1) / kAlign;
-      if (vec.size() < p1 - p0) vec.resize(p1 - p0);
-      uint64_t res = 0;
-      if (mincore(f.probe + p0 * kAlign, (p1 - p0) * kAlign, vec.data()) == 0) {
-        while (res < p1 - p0 && (vec[res] & 1)) ++res;
-      }
-      const uint64_t upto = std::min<uint64_t>(c.off + c.len, (p0 + res) * kAlign);
-      if (upto > c.off) {
-        uint64_t got = 0;
-        int err = 0;
-        if (pread_full(f.bfd, at, upto - c.off, c.off, &got, &err)) cached = got;
-      }
-    }
-    if (cached < c.len) {
-      const uint64_t from = c.off + cached;
-      const uint64_t aoff = round_down(from, kAlign);
-      const uint64_t alen = round_up(c.off + c.len, kAlign) - aoff;
-      uint8_t* dst = base + (aoff - base_off);  // 4 KiB aligned: aoff >= base_off, both aligned
-      uint64_t got = 0;
-      int err = 0;
-      bool ok = f.dfd >= 0 && pread_full(f.dfd, dst, alen, aoff, &got, &err);
-      if (ok && aoff + got < c.off + c.len) {
-        run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(aoff + got));
-        return false;
-      }
-      if (!ok && (f.dfd < 0 || err == EINVAL)) {  // no O_DIRECT on this file system: buffered
-        ok = pread_full(f.bfd, at + cached, c.len - cached, from, &got, &err);
-        if (ok && got < c.len - cached) {
-          run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(from + got));
-          return false;
-        }
-      }
-      if (!ok) {
-        run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(from) + ": " + strerror(err));
-        return false;
-      }
-      // an O_DIRECT read of a partial first / last page rewrote bytes outside
-      // the chunk with identical file contents (or slot slack): harmless
-      run->direct_bytes += c.len - cached;
-    }
-  }
-  run->buffered_bytes += cached;
-  return true;
-}
-
-// Batched chunk: wait until slot (batch mod B) holds this chunk's batch, read
-// into it, and issue the batch's single H2D copy if this was its last chunk.
-bool batched_chunk(PlanRun* run, WorkerRing& ring, const Chunk& c, std::vector<unsigned char>& vec) {
-  hl_ctx* ctx = run->ctx;
-  const Batch& bt = (*run->batches)[c.batch];
-  const int64_t nb = (int64_t)ctx->bslots.size();
-  BatchSlot& bs = ctx->bslots[c.batch % nb];
-  {
-    std::unique_lock<std::mutex> lk(ctx->bmu);
-    while (bs.batch != c.batch) {
-      if (run->failed.load()) return false;
-      if (bs.batch == c.batch - nb && bs.pending == 0) {
-        if (bs.dma) {  // the slot's previous batch is still in flight to the GPU
-          cudaEvent_t ev = bs.ev;
-          lk.unlock();
-          const double tw = now_s();
-          cudaError_t e = cudaEventSynchronize(ev);
-          run->wait_ns += (uint64_t)((now_s() - tw) * 1e9);
-          lk.lock();
-          if (e != cudaSuccess) {
-            lk.unlock();
-            run->fail(HL_ECUDA, std::string("H2D completion: ") + cudaGetErrorString(e));
-            return false;
-          }
-          if (bs.batch == c.batch - nb) bs.dma = false;
-          continue;
-        }
-        if (!bs.host) {  // first use of this slot in the context
-          const double t0 = now_s();
-          cudaError_t e = cudaHostAlloc((void**)&bs.host, ctx->bslot_bytes, cudaHostAllocPortable);
-          if (e == cudaSuccess && !bs.ev) e = cudaEventCreateWithFlags(&bs.ev, cudaEventDisableTiming);
-          {
-            std::lock_guard<std::mutex> g(run->setup_mu);
-            run->ring_setup += now_s() - t0;
-          }
-          if (e != cudaSuccess) {
-            if (bs.host) cudaFreeHost(bs.host);
-            bs.host = nullptr;
-            lk.unlock();
-            run->fail(HL_ENOMEM, std::string("pinned batch slot: ") + cudaGetErrorString(e));
-            return false;
-          }
-        }
-        bs.batch = c.batch;
-        bs.pending = bt.count;
-        ctx->bcv.notify_all();  // the batch's other chunks (and the next batch's waiters) may go on
-        break;
-      }
-      const double tw = now_s();
-      ctx->bcv.wait_for(lk, std::chrono::milliseconds(50));
-      run->wait_ns += (uint64_t)((now_s() - tw) * 1e9);
-    }
-  }
-  const double tr = now_s();
-  if (!read_chunk(run, (*run->files)[c.file], c, bs.host, bt.base, vec)) return false;
-  run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
-  std::lock_guard<std::mutex> lk(ctx->bmu);
-  if (--bs.pending == 0) {
-    const double ts = now_s();
-    cudaError_t e = cudaMemcpyAsync((void*)bt.dst, bs.host + (bt.off - bt.base), bt.len, cudaMemcpyHostToDevice,
-                                    ring.stream);
-    if (e == cudaSuccess) e = cudaEventRecord(bs.ev, ring.stream);
-    run->submit_ns += (uint64_t)((now_s() - ts) * 1e9);
-    if (e != cudaSuccess) {
-      run->err_mu.lock();
-      if (run->err_code == HL_OK) {
-        run->err_code = HL_ECUDA;
-        run->err_msg = std::string("H2D copy: ") + cudaGetErrorString(e);
-      }
-      run->failed.store(true);
-      run->err_mu.unlock();
-      ctx->bcv.notify_all();
-      return false;
-    }
-    bs.dma = true;
-    ctx->bcv.notify_all();
-  }
-  return true;
-}
-
 void worker_main(PlanRun* run, uint32_t w) {
   hl_ctx* ctx = run->ctx;
   cudaSetDevice(ctx->cfg.device);
@@ -465,10 +278,6 @@ void worker_main(PlanRun* run, uint32_t w) {
     if (i >= chunks.size()) break;
     const Chunk& c = chunks[i];
     FileState& f = files[c.file];
-    if (c.batch >= 0) {
-      if (!batched_chunk(run, ring, c, vec)) break;
-      continue;
-    }
     if (f.mode == HL_IO_CUFILE) {
       ssize_t n = g_cufile.read(f.cufh, (void*)c.dst, c.len, (off_t)c.off, 0);
       if (n < 0 || (uint64_t)n != c.len) {
@@ -531,7 +340,67 @@ void worker_main(PlanRun* run, uint32_t w) {
     // Slot layout: the chunk's bytes start at `head` = off % 4 KiB, so the
     // O_DIRECT part of any read lands 4 KiB-aligned in the slot.
     const uint64_t head = c.off % kAlign;
-    if (!read_chunk(run, f, c, s.host, c.off - head, vec)) return;
+    uint64_t cached = 0;  // leading bytes served from the page cache
+    if (f.mode == HL_IO_BUFFERED || (f.mode == HL_IO_DIRECT && f.dfd < 0)) {
+      uint64_t got = 0;
+      int err = 0;
+      if (!pread_full(f.bfd, s.host + head, c.len, c.off, &got, &err)) {
+        run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err));
+        return;
+      }
+      if (got < c.len) {
+        run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(c.off + got) + " (" +
+                              std::to_string(c.len - got) + " bytes short)");
+        return;
+      }
+      cached = c.len;
+    } else {
+      if (f.mode == HL_IO_AUTO && f.probe) {
+        // hybrid: the page-cache-resident prefix of the chunk (mincore: no I/O is
+        // triggered, unlike a RWF_NOWAIT probe whose readahead would race the
+        // O_DIRECT reads) is copied from the cache, the rest read with O_DIRECT
+        const uint64_t p0 = c.off / kAlign, p1 = (c.off + c.len + kAlign - 1) / kAlign;
+        if (vec.size() < p1 - p0) vec.resize(p1 - p0);
+        uint64_t res = 0;
+        if (mincore(f.probe + p0 * kAlign, (p1 - p0) * kAlign, vec.data()) == 0) {
+          while (res < p1 - p0 && (vec[res] & 1)) ++res;
+        }
+        const uint64_t upto = std::min<uint64_t>(c.off + c.len, (p0 + res) * kAlign);
+        if (upto > c.off) {
+          uint64_t got = 0;
+          int err = 0;
+          if (pread_full(f.bfd, s.host + head, upto - c.off, c.off, &got, &err)) cached = got;
+        }
+      }
+      if (cached < c.len) {
+        const uint64_t from = c.off + cached;
+        const uint64_t aoff = round_down(from, kAlign);
+        const uint64_t alen = round_up(c.off + c.len, kAlign) - aoff;
+        uint8_t* dst = s.host + (aoff - (c.off - head));  // 4 KiB aligned: aoff >= c.off - head
+        uint64_t got = 0;
+        int err = 0;
+        bool ok = f.dfd >= 0 && pread_full(f.dfd, dst, alen, aoff, &got, &err);
+        if (ok && aoff + got < c.off + c.len) {
+          run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(aoff + got));
+          return;
+        }
+        if (!ok && (f.dfd < 0 || err == EINVAL)) {  // no O_DIRECT on this file system: buffered
+          ok = pread_full(f.bfd, s.host + head + cached, c.len - cached, from, &got, &err);
+          if (ok && got < c.len - cached) {
+            run->fail(HL_EIO, "unexpected EOF at file offset " + std::to_string(from + got));
+            return;
+          }
+        }
+        if (!ok) {
+          run->fail(HL_EIO, std::string("read failed at offset ") + std::to_string(from) + ": " + strerror(err));
+          return;
+        }
+        // an O_DIRECT read of the partial first page rewrote bytes before `from`
+        // with identical file contents: harmless
+        run->direct_bytes += c.len - cached;
+      }
+    }
+    run->buffered_bytes += cached;
     run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
     const double ts = now_s();
     cudaError_t e = cudaMemcpyAsync((void*)c.dst, s.host + head, c.len, cudaMemcpyHostToDevice, ring.stream);
@@ -606,17 +475,6 @@ extern "C" int hl_ctx_create(const hl_config* cfg, hl_ctx** out) {
   ctx->cfg.chunk_bytes = round_up(ctx->cfg.chunk_bytes, kAlign);
   if (ctx->cfg.slots_per_worker == 0) ctx->cfg.slots_per_worker = 3;
   ctx->slot_bytes = ctx->cfg.chunk_bytes + 2 * kAlign;  // O_DIRECT head/tail slack
-  if (const char* e = getenv("HL_DMA_CHUNKS")) ctx->cfg.dma_chunks = (uint32_t)atoi(e);
-  if (ctx->cfg.dma_chunks == 0) {  // default: ~32 MiB copies (the H2D size curve flattens there)
-    ctx->cfg.dma_chunks = (uint32_t)std::max<uint64_t>(1, (32ull << 20) / ctx->cfg.chunk_bytes);
-  }
-  if (ctx->cfg.dma_chunks > 1) {
-    // same pinned budget as the per-worker rings would take: workers x slots chunks
-    const uint64_t k = ctx->cfg.dma_chunks;
-    const uint64_t nb = std::max<uint64_t>(3, (ctx->cfg.workers * (uint64_t)ctx->cfg.slots_per_worker + k - 1) / k);
-    ctx->bslots.resize(nb);
-    ctx->bslot_bytes = k * ctx->cfg.chunk_bytes + 2 * kAlign;
-  }
   ctx->rings.resize(ctx->cfg.workers);
   *out = ctx;
   return HL_OK;
@@ -639,10 +497,6 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
       if (s.host) cudaFreeHost(s.host);
     }
     if (r.stream) cudaStreamDestroy(r.stream);
-  }
-  for (auto& b : ctx->bslots) {
-    if (b.ev) cudaEventSynchronize(b.ev), cudaEventDestroy(b.ev);
-    if (b.host) cudaFreeHost(b.host);
   }
   delete ctx;
   return HL_OK;
@@ -727,9 +581,8 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     if (mode == HL_IO_AUTO && f.size) {
       void* m = mmap(nullptr, f.size, PROT_READ, MAP_SHARED, f.bfd, 0);
       if (m != MAP_FAILED) f.probe = (uint8_t*)m;
-      // AUTO copies only pages mincore found resident; kernel readahead on those
-      // preads would pull the next (cold) chunks into the cache ahead of their
-      // probes and turn the whole cold remainder into buffered reads
+      // AUTO copies only pages mincore found resident: no (synchronous) readahead
+      // on that descriptor, it would pull cold chunks in ahead of their probes
       posix_fadvise(f.bfd, 0, 0, POSIX_FADV_RANDOM);
     }
     if (mode == HL_IO_MMAP) {
@@ -770,39 +623,9 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     }
   }
 
-  // DMA batches: consecutive chunks of one contiguous range (file and device)
-  // read through the page cache or O_DIRECT share a batch slot and one copy
-  std::vector<Batch> batches;
-  if (!ctx->bslots.empty()) {
-    for (size_t i = 0; i < chunks.size(); ++i) {
-      Chunk& c = chunks[i];
-      const int m = files[c.file].mode;
-      if (m != HL_IO_BUFFERED && m != HL_IO_DIRECT && m != HL_IO_AUTO) continue;
-      if (i > 0 && chunks[i - 1].batch >= 0 && chunks[i - 1].batch == (int64_t)batches.size() - 1) {
-        Batch& b = batches.back();  // the previous chunk's batch: extend it if c continues it
-        if (chunks[i - 1].file == c.file && b.off + b.len == c.off && b.dst + b.len == c.dst &&
-            b.count < ctx->cfg.dma_chunks && round_up(c.off + c.len, kAlign) - b.base <= ctx->bslot_bytes) {
-          b.len += c.len;
-          b.count++;
-          c.batch = chunks[i - 1].batch;
-          continue;
-        }
-      }
-      batches.push_back({round_down(c.off, kAlign), c.off, c.len, c.dst, 1});
-      c.batch = (int64_t)batches.size() - 1;
-    }
-    const int64_t nb = (int64_t)ctx->bslots.size();
-    for (int64_t i = 0; i < nb; ++i) {  // slot i next hosts batch i; the previous plan's copies are done
-      ctx->bslots[i].batch = i - nb;
-      ctx->bslots[i].pending = 0;
-      ctx->bslots[i].dma = false;
-    }
-  }
-
   PlanRun run;
   run.ctx = ctx;
   run.chunks = &chunks;
-  run.batches = &batches;
   run.files = &files;
   const uint32_t nw = (uint32_t)std::min<size_t>(ctx->cfg.workers, std::max<size_t>(chunks.size(), 1));
   std::vector<std::thread> threads;

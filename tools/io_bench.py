@@ -59,8 +59,6 @@ def main():
     ap.add_argument("--chunks", default="4,16,64")
     ap.add_argument("--slots", default="3")
     ap.add_argument("--file", default=None)
-    ap.add_argument("--dma", default="0", help="dma_chunks values (0 = engine default, 1 = one copy per chunk)")
-    ap.add_argument("--no-pread-probe", action="store_true")
     args = ap.parse_args()
     if args.file:
         path = Path(args.file)
@@ -71,16 +69,14 @@ def main():
     size = path.stat().st_size
     dev = torch.empty(size, dtype=torch.uint8, device="cuda")
     _ = path.read_bytes() if size < (1 << 34) else None  # warm
-    if "buffered" in args.modes and not args.no_pread_probe:
+    if "buffered" in args.modes:
         for t in (4, 8, 12, 16):
             print(json.dumps({"probe": "pread_only_to_pinned", "threads": t, "chunk_mb": 16,
                               "GBps": round(pread_only(path, t, 16 << 20), 2)}), flush=True)
     for mode in args.modes.split(","):
         for w in map(int, args.workers.split(",")):
-            for c, sl, dm in [(float(c), int(sl), int(dm)) for c in args.chunks.split(",")
-                              for sl in args.slots.split(",") for dm in args.dma.split(",")]:
-                eng = _native.IoEngine(0, workers=w, chunk_bytes=int(c * (1 << 20)), slots_per_worker=sl, io_mode=mode,
-                                       dma_chunks=dm)
+            for c, sl in [(float(c), int(sl)) for c in args.chunks.split(",") for sl in args.slots.split(",")]:
+                eng = _native.IoEngine(0, workers=w, chunk_bytes=int(c * (1 << 20)), slots_per_worker=sl, io_mode=mode)
                 res = []
                 for i in range(3):
                     if mode == "direct":
@@ -88,10 +84,8 @@ def main():
                     st = eng.execute([str(path)], [(0, 0, 0, size, dev.data_ptr())])
                     if i:
                         res.append(size / st["seconds"] / 1e9)
-                eng_cfg = eng.config
                 eng.close()
-                print(json.dumps({"mode": mode, "workers": w, "chunk_mb": c, "slots": sl,
-                                  "dma_chunks": eng_cfg["dma_chunks"], "GBps": round(max(res), 2),
+                print(json.dumps({"mode": mode, "workers": w, "chunk_mb": c, "slots": sl, "GBps": round(max(res), 2),
                                   "modes_used": st["io_modes"], "ring_setup_s": round(st["ring_setup_seconds"], 4),
                                   "read_s": round(st["read_seconds"], 3), "wait_s": round(st["wait_seconds"], 3),
                                   "submit_s": round(st["submit_seconds"], 3), "wall_s": round(st["seconds"], 3)}),
