@@ -77,6 +77,11 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kUnroll = 8;
 constexpr uint64_t kUnitVecs = 32 * kUnroll;   // 4 KiB of output per warp unit
+// Row units of the bf16 -> f32 widening (8-byte source spans, a shift per
+// element) are twice as long and run with twice the unroll, so a lane keeps
+// as many source bytes in flight as the copy kernel (16 x 8 B, not 8 x 8 B).
+// (f16 -> f32 keeps 8: its NaN-preserving conversion would need ~100 registers.)
+__host__ __device__ constexpr uint64_t row_unit_vecs(int kind) { return kind == 4 ? 2 * kUnitVecs : kUnitVecs; }
 constexpr uint64_t kUnitElems = 32 * kUnroll;  // elements per unit on the element path
 
 constexpr int kSmallDescs = 4;  // single-key calls launch with a 240-byte parameter block
@@ -400,7 +405,7 @@ __device__ __forceinline__ void row_unit(const uint8_t* rsrc, uint8_t* rdst, uin
   constexpr int NB = KindTraits<K>::NB;
   constexpr int G = NB >= 16 ? 16 : 8;  // granule
   constexpr int W = NB / G;             // granules per span (1 or 2)
-  constexpr int U = (W == 2) ? kUnroll / 2 : kUnroll;
+  constexpr int U = (W == 2) ? kUnroll / 2 : (K == K_BF16_F32 ? 2 * kUnroll : kUnroll);
   const uintptr_t a = reinterpret_cast<uintptr_t>(rsrc);
   const uint32_t sh = a & (G - 1);
   if (RC == R_ALIGNED || (RC == R_MIXED && sh == 0)) {
@@ -513,8 +518,9 @@ __global__ void __launch_bounds__(kThreads) row_kernel(const __grid_constant__ P
     const KDesc& d = p.d[di];
     const uint32_t lu = (uint32_t)(u - d.unit_begin);  // < 2^32 units (16 TiB) per descriptor
     const uint32_t row = lu / d.upr;
-    const uint64_t v0 = (uint64_t)(lu - row * d.upr) * kUnitVecs;
-    const uint64_t v1 = min(v0 + kUnitVecs, d.row_len);
+    constexpr uint64_t UV = row_unit_vecs(K);
+    const uint64_t v0 = (uint64_t)(lu - row * d.upr) * UV;
+    const uint64_t v1 = min(v0 + UV, d.row_len);
     const uint8_t* rsrc = reinterpret_cast<const uint8_t*>(d.src) + (uint64_t)row * d.src_pitch + v0 * NB;
     uint8_t* rdst = reinterpret_cast<uint8_t*>(d.dst) + ((uint64_t)row * d.row_len + v0) * 16;
     row_unit<K, RC>(rsrc, rdst, (uint32_t)(v1 - v0), lane);
@@ -638,7 +644,8 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
       k.nvec = rows * vpr;
       if (rows == 1 || vpr >= kMinRowVecs) {
         k.mode = M_ROWS;
-        k.upr = (uint32_t)((vpr + kUnitVecs - 1) / kUnitVecs);
+        const uint64_t uv = row_unit_vecs(kind);
+        k.upr = (uint32_t)((vpr + uv - 1) / uv);
         units[*count] = rows * k.upr;
         const uint64_t g = (kind == K_F16_F32 || kind == K_BF16_F32) ? 8 : 16;  // load granule
         const bool uniform = rows == 1 || pitch % g == 0;
