@@ -25,7 +25,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .format import DType, FileHeader, write_file_stream
+from .format import DType, write_file_stream
 
 Entry = tuple[str, DType, tuple[int, ...]]
 

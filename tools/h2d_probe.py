@@ -2,7 +2,6 @@
 engine in isolation): 8 GiB per point from a pinned pool into one device
 buffer, copies round-robin over S streams."""
 import json
-import sys
 
 import torch
 
