@@ -652,6 +652,9 @@ def main():
                     "traffic": traffic, "kernel": "hl_gather row_kernel<"
                     + (f"{src_dt.value}->{cast.value}" if cast else "K_COPY1") + ", aligned>",
                     "launches_per_step": k_n, "algorithmic_bytes_per_launch": k_bytes // max(k_n, 1),
+                    # live: the kernel's share of the value step (the rest is host pre-launch work);
+                    # ncu's launch list has this launch as the step's only GPU work (profiles/)
+                    "kernel_share_of_step": round(k_ms / max(value_ms, 1e-9), 4) if k_n else None,
                     "peak_source": peak_source}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
