@@ -403,3 +403,22 @@ def test_get_tensors_batched_matches_per_key(tmp_path, rng):
     with pytest.raises(BadDim):
         fb.get_tensors([keys[0]], dims={keys[0]: 9})
     fb.close()
+
+
+def test_upstream_spellings_as_dict_filename_shape(tmp_path, rng):
+    """fastsafetensors' own FilesBufferOnDevice spellings (superset): as_dict
+    with dim -1 = full tensor, get_filename, get_shape."""
+    t = random_tensor_set(rng, 6, prefix="u", dtypes=[DType.BF16, DType.F32])
+    p = _write(tmp_path, "u.safetensors", t)
+    loader = SafeTensorsFileLoader(SingleGroup(), "host")
+    loader.add_filenames({0: [p]})
+    fb = loader.copy_files_to_device()
+    keys = sorted(t)
+    assert fb.get_filename(keys[0]) == str(p) and fb.get_filename("missing") == ""
+    assert fb.get_shape(keys[1]) == list(t[keys[1]][1])
+    req = {k: (-1 if i % 2 else 0) for i, k in enumerate(keys) if t[k][1] and t[k][1][0] >= 1}
+    got = fb.as_dict(req)
+    assert list(got) == list(req)
+    for k in req:
+        assert got[k].tobytes() == t[k][2]  # world 1: every shard is the full tensor
+    fb.close()
