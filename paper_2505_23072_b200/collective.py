@@ -318,10 +318,43 @@ class DistGroup:
             hosts = self.exchange(self.rank, socket.gethostname()) if self.world_size > 1 else {0: ""}
             one_node = len(set(hosts.values())) == 1
             data_plane = "ipc" if (one_node and self.device.type == "cuda") else "nccl"
+            if data_plane == "ipc" and self.world_size > 1 and not self._ipc_works():
+                data_plane = "nccl"  # e.g. a container without IPC rights: the same path over NCCL
         self.data_plane = data_plane
 
     def rank_ids(self) -> range:
         return range(self.world_size)
+
+    def _ipc_works(self) -> bool:
+        """Probe the peer-memory plane once: every rank maps its right
+        neighbour's allocation through CUDA IPC and reads it with one hl_gather
+        launch. Collective; True only if it worked on every rank."""
+        from . import _native
+
+        probe = torch.full((4096,), (self.rank + 1) % 256, dtype=torch.uint8, device=self.device)
+        torch.cuda.synchronize(self.device)
+        try:
+            mine = _native.ipc_export(probe.data_ptr())
+        except Exception:  # noqa: BLE001 - any failure means: use NCCL
+            mine = None
+        handles = self.exchange(self.rank, mine)
+        peer = (self.rank + 1) % self.world_size
+        ok, ptr = False, None
+        try:
+            if handles[peer] is not None:
+                ptr = _native.ipc_import(handles[peer], self.device.index)
+                out = torch.zeros(4096, dtype=torch.uint8, device=self.device)
+                kernels.run([kernels.copy_desc(ptr, out.data_ptr(), 4096, DType.U8)], self.device)
+                torch.cuda.synchronize(self.device)
+                ok = bool((out == (peer + 1) % 256).all().item())
+        except Exception:  # noqa: BLE001
+            ok = False
+        finally:
+            if ptr is not None:
+                _native.ipc_release(ptr)
+        verdict = all(self.exchange(self.rank, ok).values())  # also keeps every probe alive until read
+        del probe
+        return verdict
 
     # -- peer-memory data plane ("ipc") --------------------------------------------------
     def publish(self, buffers: dict[str, int], device_index: int) -> dict[str, int]:

@@ -179,3 +179,17 @@ def features_job(rank, world):
 def test_ipc_plane_casts_dims_repeats(world):
     for rank_result in _run(world, features_job):
         assert all(rank_result.values()), rank_result
+
+
+def auto_plane_job(rank, world):
+    """data_plane="auto" probes CUDA IPC once (every rank maps its neighbour's
+    probe allocation and reads it with hl_gather) and settles on "ipc" here."""
+    from paper_2505_23072_b200 import DistGroup
+
+    g = DistGroup(device=torch.device("cuda", 0))
+    return {"plane": g.data_plane}
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_auto_plane_probes_ipc(world):
+    assert [r["plane"] for r in _run(world, auto_plane_job)] == ["ipc"] * world
