@@ -67,7 +67,8 @@ enum hl_dtype {
 
 /* ---- I/O modes ----------------------------------------------------------------- */
 enum hl_io_mode {
-  HL_IO_AUTO = 0,      /* per file: buffered if mostly page-cache resident, else O_DIRECT */
+  HL_IO_AUTO = 0,      /* per chunk: the page-cache-resident prefix (mincore) buffered,
+                          the rest O_DIRECT                                             */
   HL_IO_BUFFERED = 1,  /* pread through the page cache into the pinned ring            */
   HL_IO_DIRECT = 2,    /* O_DIRECT pread (4 KiB aligned) into the pinned ring            */
   HL_IO_CUFILE = 3,    /* cuFileRead straight into HBM (GPUDirect Storage, nvidia-fs)    */
@@ -193,7 +194,7 @@ int hl_conversion_supported(uint32_t src_dtype, uint32_t dst_dtype);
 int hl_gather(const hl_desc* descs, uint32_t n, void* stream);
 uint32_t hl_gather_max_batch(void);
 
-/* Number of kernel launches hl_gather issued on this thread so far. */
+/* Number of kernel launches hl_gather issued by this process so far. */
 uint64_t hl_kernel_launches(void);
 
 #ifdef __cplusplus

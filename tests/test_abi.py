@@ -91,3 +91,47 @@ def test_missing_library_is_an_error(tmp_path):
             "try:\n  n.load()\nexcept Exception as e:\n  print(type(e).__name__)\n")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT).stdout
     assert "NativeUnavailable" in out
+
+
+CUDA = "/usr/local/cuda"
+
+
+def _build_c_smoke(out_dir):
+    exe = out_dir / "abi_smoke"
+    cmd = ["gcc", "-O2", "-Wall", "-Werror", "-std=c11", f"-I{ROOT / 'include'}", f"-I{CUDA}/include",
+           str(ROOT / "tests" / "c" / "abi_smoke.c"), "-o", str(exe),
+           f"-L{_native.LIB_PATH.parent}", "-lhbmload", f"-L{CUDA}/lib64", "-lcudart",
+           f"-Wl,-rpath,{_native.LIB_PATH.parent}:{CUDA}/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_program_builds_against_the_header(tmp_path):
+    """A plain C11 host (no Python, no torch) compiles and links against
+    include/hbmload.h + libhbmload.so: the boundary is self-contained."""
+    _build_c_smoke(tmp_path)
+
+
+@pytest.mark.gpu
+def test_c_program_loads_realigns_casts_and_shards(tmp_path, rng):
+    import numpy as np
+
+    exe = _build_c_smoke(tmp_path)
+    raw = rng.integers(0, 256, size=(1 << 20) + 37, dtype=np.uint8)
+    src = tmp_path / "blob.bin"
+    src.write_bytes(raw.tobytes())
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), str(src), str(out)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "error path ok" in r.stdout
+    launches = int(re.search(r"launches (\d+)", r.stdout).group(1))
+    assert 1 <= launches <= 3  # one per (conversion kind, kernel variant) present in the batch
+    got = out.read_bytes()
+    nb, nc, rows, cols, lo, hi = 100003, 65536, 37, 300, 100, 200
+    b = raw[3:3 + nb].tobytes()
+    c = oracle.convert(raw[16:16 + 2 * nc].tobytes(), "BF16", "F16")
+    d = raw[64:64 + rows * cols * 2].reshape(rows, cols * 2)[:, lo * 2:hi * 2].tobytes()
+    assert got[:nb] == b
+    assert got[nb:nb + len(c)] == c
+    assert got[nb + len(c):] == d
