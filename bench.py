@@ -515,7 +515,7 @@ def main():
         return fb
 
     kernels.TIMING = []
-    vals = []
+    vals, dom_ms, dom_bytes = [], [], 0
     launches_value = 0
     for i in range(args.warmup + args.steps):
         fb = fresh_fb()
@@ -535,6 +535,10 @@ def main():
             k_ms = sum(a.elapsed_time(b) for a, b, _ in kernels.TIMING)
             k_bytes = sum(nb for _, _, nb in kernels.TIMING)
             k_n = len(kernels.TIMING)
+            # the dominant launch of the step (get_tensors issues a small head group first)
+            a_, b_, nb_ = max(kernels.TIMING, key=lambda t: t[2])
+            dom_ms.append(a_.elapsed_time(b_))
+            dom_bytes = nb_
         del outs
         torch.cuda.synchronize()
         barrier()  # every rank is done reading peers' landed buffers
@@ -544,7 +548,8 @@ def main():
     value_ms = statistics.median(vals)
     value = job_bytes / (value_ms / 1e3) / 1e9
     hbm_peak, peak_source = hbm_peak_gbs()
-    achieved = (k_bytes / max(k_n, 1)) / ((k_ms / max(k_n, 1)) / 1e3) / 1e9 if k_n else None
+    achieved = dom_bytes / (statistics.mean(dom_ms) / 1e3) / 1e9 if dom_ms else None
+    achieved_all = k_bytes / (k_ms / 1e3) / 1e9 if k_n else None
     traffic = None
     tr_file = ROOT / "profiles" / "ncu_traffic.json"
     if tr_file.exists():
@@ -651,7 +656,8 @@ def main():
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
                     "traffic": traffic, "kernel": "hl_gather row_kernel<"
                     + (f"{src_dt.value}->{cast.value}" if cast else "K_COPY1") + ", aligned>",
-                    "launches_per_step": k_n, "algorithmic_bytes_per_launch": k_bytes // max(k_n, 1),
+                    "launches_per_step": k_n, "algorithmic_bytes_per_launch": dom_bytes,
+                    "achieved_all_launches_of_step": round(achieved_all, 1) if achieved_all else None,
                     # live: the kernel's share of the value step (the rest is host pre-launch work);
                     # ncu's launch list has this launch as the step's only GPU work (profiles/)
                     "kernel_share_of_step": round(k_ms / max(value_ms, 1e-9), 4) if k_n else None,
