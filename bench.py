@@ -139,6 +139,27 @@ def warm_cache(paths, threads: int = 16, chunk: int = 64 << 20) -> None:
         t.join()
 
 
+def residency(paths) -> float:
+    """Byte-weighted page-cache residency of the files (mincore)."""
+    from paper_2505_23072_b200 import _native
+
+    sizes = [os.path.getsize(p) for p in paths]
+    return round(sum(_native.file_residency(str(p)) * n for p, n in zip(paths, sizes)) / max(sum(sizes), 1), 4)
+
+
+def host_memory() -> dict:
+    """MemTotal / MemAvailable / Cached in GB (/proc/meminfo)."""
+    out = {}
+    try:
+        for line in open("/proc/meminfo"):
+            k, v = line.split(":")
+            if k in ("MemTotal", "MemAvailable", "Cached"):
+                out[k] = round(int(v.split()[0]) / 1e6, 1)
+    except OSError:
+        pass
+    return out
+
+
 def drop_cache(paths):
     from paper_2505_23072_b200 import _native
 
@@ -600,6 +621,8 @@ def main():
     e2e_ms, launches_e2e, io_modes, h2d_bytes, ring = [], 0, set(), 0, 0.0
     first_ms = None
     warm_cache(mapping[rank])  # "warm" means resident: O_DIRECT reads of a cold file would not make it so
+    host_mem = host_memory()
+    resid = {"after_warm": residency(mapping[rank])}
     for i in range(args.warmup):
         ms, _, _ = e2e_step()
         if first_ms is None:
@@ -615,6 +638,7 @@ def main():
             h2d_bytes = st.bytes
             ring = max(ring, st.ring_setup_seconds)
     clk = clocks.stop()
+    resid["after_warm_steps"] = residency(mapping[rank])
     phase_med = {k: round(statistics.median(p[k] for p in phases[-args.steps:]), 2) for k in phases[-1]}
     e2e_med = statistics.median(e2e_ms)
     e2e_val = job_bytes / (e2e_med / 1e3) / 1e9
@@ -676,6 +700,7 @@ def main():
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "seconds_to_ready": round(e2e_med / 1e3, 4),
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h, "page_cache": "warm",
                     "io_modes": sorted(io_modes), "ring_setup_seconds_first_load": round(ring, 4),
+                    "page_cache_residency": resid, "host_memory_gb": host_mem,
                     "first_load_seconds_in_process": round(first_ms / 1e3, 4) if first_ms else None,
                     "phases_ms": phase_med},
             "e2e_cold": cold,
