@@ -119,6 +119,31 @@ def _source_ptr(view, device: torch.device) -> int:
     return view.buffer.ptr + view.base_offset, None
 
 
+def pack_parts(spec: ShardSpec, src_ptr: int, in_dtype: DType, out_dtype: DType, own: int,
+               own_out: torch.Tensor, device: torch.device) -> list[torch.Tensor]:
+    """Owner-side pack of the NCCL scatter: every rank's slice of the tensor at
+    ``src_ptr`` (cast to ``out_dtype``) with ONE hl_gather launch — the owner's
+    own slice straight into ``own_out``, the others into one pack buffer with
+    16-byte aligned parts. Returns the W uint8 parts, enqueued on the current
+    stream (ref collective.py:214-255 / 318-330)."""
+    esz = out_dtype.size_bytes
+    sizes = [math.prod(p) * esz for p in spec.part_shapes]
+    pack_bytes = sum(-(-sz // 16) * 16 for r, sz in enumerate(sizes) if r != own)
+    pack = torch.empty(pack_bytes + 16, dtype=torch.uint8, device=device)
+    parts, descs, cursor = [], [], 0
+    for r in range(spec.world_size):
+        lo, hi = spec.bounds(r)
+        if r == own:
+            dst, part = own_out.data_ptr(), own_out
+        else:
+            dst, part = pack.data_ptr() + cursor, pack[cursor : cursor + sizes[r]]
+            cursor += -(-sizes[r] // 16) * 16  # keep every part 16-byte aligned
+        descs.append(kernels.shard_desc(src_ptr, spec.full_shape, spec.dim, lo, hi, dst, in_dtype, out_dtype))
+        parts.append(part)
+    kernels.run(descs, device)
+    return parts
+
+
 # ------------------------------------------------------------------------ thread group
 @dataclass(frozen=True)
 class _Span:
@@ -491,7 +516,6 @@ class DistGroup:
         if in_dtype is None:
             raise ValueError("receivers must know the source dtype (src_dtype)")
         out_dtype = dtype or in_dtype
-        esz = out_dtype.size_bytes
         buf, out = _fresh(pool, tag or spec.key, out_dtype, spec.part_shapes[rank])
         mine = buf.tensor[: out.nbytes]
         if rank != src:
@@ -501,20 +525,7 @@ class DistGroup:
             raise SpecMismatch(f"scatter src rank {src} holds no view (tag={tag!r})")
         if tuple(source_view.shape) != spec.full_shape:
             raise SpecMismatch(f"source shape {list(source_view.shape)} does not match spec {list(spec.full_shape)}")
-        sizes = [math.prod(p) * esz for p in spec.part_shapes]
-        pack_bytes = sum(-(-sz // 16) * 16 for r, sz in enumerate(sizes) if r != src)
-        pack = torch.empty(pack_bytes + 16, dtype=torch.uint8, device=pool.device)
-        src_ptr = source_view.buffer.ptr + source_view.base_offset
-        parts, descs, cursor = [], [], 0
-        for r in range(self.world_size):
-            lo, hi = spec.bounds(r)
-            if r == src:
-                dst, part = buf.ptr, mine
-            else:
-                dst, part = pack.data_ptr() + cursor, pack[cursor : cursor + sizes[r]]
-                cursor += -(-sizes[r] // 16) * 16  # keep every part 16-byte aligned
-            descs.append(kernels.shard_desc(src_ptr, spec.full_shape, spec.dim, lo, hi, dst, in_dtype, out_dtype))
-            parts.append(part)
-        kernels.run(descs, pool.device)
+        parts = pack_parts(spec, source_view.buffer.ptr + source_view.base_offset, in_dtype, out_dtype,
+                           own=src, own_out=mine, device=pool.device)
         self.scatter_parts(rank, src, parts, mine)
         return out
