@@ -463,18 +463,25 @@ class DistGroup:
         dist = self._dist
         if self.world_size == 1:
             return
-        ops = []
+        # gloo moves CUDA tensors in collectives but not point-to-point: stage
+        # through host memory there (NCCL sends device memory directly)
+        stage = self.backend == "gloo" and out.is_cuda
+        ops, landing = [], out
         if rank == src:
             if parts is None or len(parts) != self.world_size:
                 raise SpecMismatch("scatter owner must provide one part per rank")
             for r in range(self.world_size):
                 if r != src and parts[r].numel():
-                    ops.append(dist.P2POp(dist.isend, parts[r], self._global(r), group=self.pg))
+                    ops.append(dist.P2POp(dist.isend, parts[r].cpu() if stage else parts[r], self._global(r),
+                                          group=self.pg))
         elif out.numel():
-            ops.append(dist.P2POp(dist.irecv, out, self._global(src), group=self.pg))
+            landing = torch.empty(out.shape, dtype=out.dtype) if stage else out
+            ops.append(dist.P2POp(dist.irecv, landing, self._global(src), group=self.pg))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+        if landing is not out:
+            out.copy_(landing)
 
     # -- TensorView level (what the loader calls; same signatures as ProcessGroup) -------------
     def broadcast(self, rank: int, view, src: int, pool=None, tag: str = "", meta=None):

@@ -1,4 +1,6 @@
-"""The peer-memory data plane across real processes (DistGroup(data_plane="ipc")).
+"""The multi-GPU data planes across real processes (DistGroup).
+
+ipc: the peer-memory plane (the default on one node).
 
 W processes share the box's one B200 (CUDA IPC works between processes on the
 same device; the control plane is gloo on 127.0.0.1). Every rank lands only
@@ -7,6 +9,10 @@ get_sharded is ONE hl_gather launch per rank reading the owner's HBM through
 the IPC mapping — on a multi-GPU box the same reads travel over NVLink.
 Results are checked against the reference loader's own outputs
 (tests/golden/corpora/expect.json) and the oracle.
+
+nccl: the collective plane (owner pack kernel + broadcast / grouped
+send-recv). NCCL refuses two ranks on one GPU, so gloo stands in for it here:
+the same calls, gloo moving the CUDA tensors (P2P staged through the host).
 """
 
 from __future__ import annotations
@@ -70,14 +76,14 @@ def _run(world, job, timeout=240):
     return [res[r] for r in range(world)]
 
 
-def golden_job(rank, world):
-    """Every golden case of this world size through the ipc data plane."""
+def golden_job(rank, world, plane="ipc"):
+    """Every golden case of this world size through the given data plane."""
     import json
 
     from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader
 
     cases = [c for c in json.loads((CORPORA / "expect.json").read_text())["cases"] if c["world"] == world]
-    group = DistGroup(device=torch.device("cuda", 0), data_plane="ipc", check_order=True)
+    group = DistGroup(device=torch.device("cuda", 0), data_plane=plane, check_order=True)
     out = {}
     for case in cases:
         mapping = {int(r): [str(CORPORA / f) for f in fs] for r, fs in case["mapping"].items()}
@@ -106,7 +112,21 @@ def test_ipc_plane_matches_reference_loader(world):
         assert rank_result and all(rank_result.values()), rank_result
 
 
-def features_job(rank, world):
+def golden_job_collective_plane(rank, world):
+    return golden_job(rank, world, plane="nccl")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.timeout(600)
+def test_collective_plane_matches_reference_loader(world):
+    """The NCCL data plane's whole flow (owner pack kernel, broadcast, grouped
+    send/recv, repeated/stale keys) with gloo standing in for NCCL — NCCL
+    refuses two ranks on one GPU, and the box has one."""
+    for rank_result in _run(world, golden_job_collective_plane):
+        assert rank_result and all(rank_result.values()), rank_result
+
+
+def features_job(rank, world, plane="ipc"):
     """dtype casts, Megatron dims on a larger checkpoint slice, repeated keys
     (buffer still alive, then from a surviving tensor), stale shards."""
     import numpy as np
@@ -130,7 +150,7 @@ def features_job(rank, world):
                 f.write(write_file(t, pad_header_to=301 + i))  # odd bodies: realign on simdirect
         files.append((p, t))
     torch.distributed.barrier()
-    group = DistGroup(device=torch.device("cuda", 0), data_plane="ipc")
+    group = DistGroup(device=torch.device("cuda", 0), data_plane=plane)
     loader = SafeTensorsFileLoader(group, "simdirect")
     loader.add_filenames({r: [files[r][0]] for r in range(world)})
     fb = loader.copy_files_to_device()
@@ -164,7 +184,8 @@ def features_job(rank, world):
     dims = {k: (0 if k.endswith("q") else 1) for k in keys if not k.endswith("n")}
     l0 = _native.kernel_launches()
     got = fb.get_tensors(keys, dims=dims)
-    ok["batch_launches"] = _native.kernel_launches() - l0 <= 3  # one per conversion kind present
+    if plane == "ipc":  # the collective plane serves a batch key by key
+        ok["batch_launches"] = _native.kernel_launches() - l0 <= 3  # one per conversion kind present
     for i, (p, t) in enumerate(files):
         ok[f"bq{i}"] = got[f"l{i}.q"].tobytes() == oracle.slice_bytes(t[f"l{i}.q"][2], "BF16", (256, 192), 0, world, rank)[1]
         ok[f"bo{i}"] = got[f"l{i}.o"].tobytes() == oracle.slice_bytes(t[f"l{i}.o"][2], "F32", (96, 130), 1, world, rank)[1]
@@ -178,6 +199,16 @@ def features_job(rank, world):
 @pytest.mark.timeout(600)
 def test_ipc_plane_casts_dims_repeats(world):
     for rank_result in _run(world, features_job):
+        assert all(rank_result.values()), rank_result
+
+
+def features_job_collective_plane(rank, world):
+    return features_job(rank, world, plane="nccl")
+
+
+@pytest.mark.timeout(600)
+def test_collective_plane_casts_dims_repeats():
+    for rank_result in _run(3, features_job_collective_plane):
         assert all(rank_result.values()), rank_result
 
 
