@@ -18,9 +18,10 @@
 // cuFile's own compat mode otherwise), loaded with dlopen so the library
 // has no hard dependency on libcufile.
 //
-// The ring is allocated once per context (lazily, inside the workers so the
-// pages are first-touched on the workers' NUMA node) and reused by every
-// later plan; its cost is reported in hl_plan_stats.ring_setup_seconds.
+// The ring is one pinned region per context (huge-page backed, first-touched
+// on the GPU's NUMA node, see ensure_ring_memory), allocated before the first
+// plan's workers start and reused by every later plan; its cost is reported in
+// hl_plan_stats.ring_setup_seconds.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdlib.h>
@@ -161,6 +162,9 @@ struct hl_ctx {
   std::vector<WorkerRing> rings;
   bool ring_ready = false;
   uint64_t slot_bytes = 0;
+  uint8_t* ring_mem = nullptr;  // every worker's slots, one pinned region
+  uint64_t ring_bytes = 0;
+  bool ring_registered = false;  // cudaHostRegister'ed malloc (else cudaHostAlloc)
   std::mutex mu;  // one plan at a time per context
 };
 
@@ -222,9 +226,53 @@ bool pread_full(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got,
   return true;
 }
 
-// Stream + event per slot now; the pinned memory of a slot is allocated the
-// first time the slot is used, so a fresh process starts reading into slot 0
-// while the other slots do not exist yet (their allocation overlaps I/O).
+// The pinned memory of every worker's slots is ONE region, allocated before
+// the first plan's workers start: 2 MiB-aligned, transparent-huge-page backed,
+// first-touched by a thread on the GPU's NUMA node, then registered with
+// cudaHostRegister. Measured on the B200 box (tools/pinned_probe.cu): 21 ms for
+// 144 MiB, vs 74 ms for 36 separate cudaHostAlloc calls — and slot-by-slot
+// allocation during the first load stalled behind the in-flight copies (first
+// load 0.73 s vs 0.27 s steady; profiles/r01_first_load.jsonl).
+int ensure_ring_memory(hl_ctx* ctx, double* seconds) {
+  if (ctx->ring_mem) return HL_OK;
+  const double t0 = now_s();
+  const uint64_t bytes = round_up((uint64_t)ctx->cfg.workers * ctx->cfg.slots_per_worker * ctx->slot_bytes, 2ull << 20);
+  void* m = nullptr;
+  bool registered = false;
+  if (posix_memalign(&m, 2ull << 20, bytes) == 0) {
+    madvise(m, bytes, MADV_HUGEPAGE);
+    std::thread toucher([&] {  // first touch on the GPU's NUMA node
+      if (!ctx->cpus.empty()) {
+        cpu_set_t set;
+        CPU_ZERO(&set);
+        for (int c : ctx->cpus) CPU_SET(c, &set);
+        sched_setaffinity(0, sizeof set, &set);
+      }
+      memset(m, 0, bytes);
+    });
+    toucher.join();
+    if (cudaHostRegister(m, bytes, cudaHostRegisterPortable) == cudaSuccess) {
+      registered = true;
+    } else {
+      cudaGetLastError();
+      free(m);
+      m = nullptr;
+    }
+  }
+  if (!m) {
+    cudaError_t e = cudaHostAlloc(&m, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      return set_error(HL_ENOMEM, "pinned ring of %llu bytes: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    }
+  }
+  ctx->ring_mem = (uint8_t*)m;
+  ctx->ring_bytes = bytes;
+  ctx->ring_registered = registered;
+  *seconds = now_s() - t0;
+  return HL_OK;
+}
+
+// Stream + event per slot; slot memory comes from the context's pinned region.
 int ensure_ring(hl_ctx* ctx, WorkerRing& r) {
   if (!r.slots.empty()) return HL_OK;
   cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
@@ -237,14 +285,10 @@ int ensure_ring(hl_ctx* ctx, WorkerRing& r) {
   return HL_OK;
 }
 
-int ensure_slot(hl_ctx* ctx, Slot& s) {
+int ensure_slot(hl_ctx* ctx, uint32_t w, uint32_t k, Slot& s) {
   if (s.host) return HL_OK;
-  cudaError_t e = cudaHostAlloc((void**)&s.host, ctx->slot_bytes, cudaHostAllocPortable);
-  if (e != cudaSuccess) {
-    s.host = nullptr;
-    return set_error(HL_ENOMEM, "pinned slot of %llu bytes: %s", (unsigned long long)ctx->slot_bytes,
-                     cudaGetErrorString(e));
-  }
+  if (!ctx->ring_mem) return set_error(HL_ENOMEM, "pinned ring not allocated");
+  s.host = ctx->ring_mem + ((uint64_t)w * ctx->cfg.slots_per_worker + k) * ctx->slot_bytes;
   return HL_OK;
 }
 
@@ -325,12 +369,7 @@ void worker_main(PlanRun* run, uint32_t w) {
       cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
     }
     if (!s.host) {
-      const double t0 = now_s();
-      int rc = ensure_slot(ctx, s);
-      {
-        std::lock_guard<std::mutex> g(run->setup_mu);
-        run->ring_setup += now_s() - t0;
-      }
+      int rc = ensure_slot(ctx, w, (uint32_t)(&s - ring.slots.data()), s);
       if (rc) {
         run->fail(rc, hl_last_error());
         return;
@@ -494,9 +533,16 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
     if (r.stream) cudaStreamSynchronize(r.stream);
     for (auto& s : r.slots) {
       if (s.ev) cudaEventDestroy(s.ev);
-      if (s.host) cudaFreeHost(s.host);
     }
     if (r.stream) cudaStreamDestroy(r.stream);
+  }
+  if (ctx->ring_mem) {
+    if (ctx->ring_registered) {
+      cudaHostUnregister(ctx->ring_mem);
+      free(ctx->ring_mem);
+    } else {
+      cudaFreeHost(ctx->ring_mem);
+    }
   }
   delete ctx;
   return HL_OK;
@@ -627,6 +673,15 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
   run.ctx = ctx;
   run.chunks = &chunks;
   run.files = &files;
+  {
+    double secs = 0;
+    int rc = ensure_ring_memory(ctx, &secs);
+    if (rc) {
+      close_all();
+      return rc;
+    }
+    run.ring_setup += secs;
+  }
   const uint32_t nw = (uint32_t)std::min<size_t>(ctx->cfg.workers, std::max<size_t>(chunks.size(), 1));
   std::vector<std::thread> threads;
   threads.reserve(nw);
