@@ -61,3 +61,20 @@ def test_llama_logits_match_safetensors(ckpt, batched):
         b = m(tokens).logits
     assert torch.isfinite(a).all()
     assert torch.equal(a, b)
+
+
+def test_vllm_weights_iterator_matches_safetensors(ckpt):
+    """The vLLM load-format hook yields every (name, tensor) of the
+    checkpoint on the GPU, bit-identical to safetensors."""
+    from safetensors.torch import load_file
+
+    from paper_2505_23072_b200.vllm_loader import weights_iterator
+
+    ref = {}
+    for p in ckpt:
+        ref.update(load_file(str(p), device="cuda:0"))
+    seen = {}
+    for name, t in weights_iterator([str(p) for p in ckpt]):
+        assert t.is_cuda and t.dtype == ref[name].dtype and t.shape == ref[name].shape
+        seen[name] = torch.equal(t.view(torch.int16), ref[name].view(torch.int16))
+    assert set(seen) == set(ref) and all(seen.values())
