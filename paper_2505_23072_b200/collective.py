@@ -483,6 +483,31 @@ class DistGroup:
         if landing is not out:
             out.copy_(landing)
 
+    def p2p(self, ops: list[tuple[str, torch.Tensor, int]]) -> None:
+        """One grouped point-to-point call for a whole batch (ncclGroupStart /
+        ncclGroupEnd under torch's batch_isend_irecv): ``ops`` are
+        ("send" | "recv", contiguous tensor, group rank), posted in the same
+        key order on every rank. gloo cannot move CUDA tensors point to point,
+        so there they are staged through host memory."""
+        if not ops or self.world_size == 1:
+            return
+        dist = self._dist
+        stage = self.backend == "gloo"
+        staged, posted = [], []
+        for kind, t, peer in ops:
+            h = t
+            if stage and t.is_cuda:
+                if kind == "send":
+                    h = t.cpu()
+                else:
+                    h = torch.empty(t.shape, dtype=t.dtype)
+                    staged.append((t, h))
+            posted.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, h, self._global(peer), group=self.pg))
+        for w in dist.batch_isend_irecv(posted):
+            w.wait()
+        for t, h in staged:
+            t.copy_(h)
+
     # -- TensorView level (what the loader calls; same signatures as ProcessGroup) -------------
     def broadcast(self, rank: int, view, src: int, pool=None, tag: str = "", meta=None):
         """ncclBroadcast from ``src``; receivers allocate from their own pool.

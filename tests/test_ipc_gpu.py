@@ -76,8 +76,9 @@ def _run(world, job, timeout=240):
     return [res[r] for r in range(world)]
 
 
-def golden_job(rank, world, plane="ipc"):
-    """Every golden case of this world size through the given data plane."""
+def golden_job(rank, world, plane="ipc", batched=False):
+    """Every golden case of this world size through the given data plane,
+    key by key or as one get_tensors batch per case."""
     import json
 
     from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader
@@ -92,13 +93,14 @@ def golden_job(rank, world, plane="ipc"):
             loader.add_filenames(mapping)
             fb = loader.copy_files_to_device()
             got = {}
-            for k in sorted(fb.keys()):
-                m = fb.metadata(k)
-                if case["dim"] < len(m.shape) and m.shape[case["dim"]] >= world:
-                    v, kind = fb.get_sharded(k, case["dim"]), "shard"
-                else:
-                    v, kind = fb.get_tensor(k), "full"
-                got[k] = [kind, list(v.shape), hashlib.sha256(v.tobytes()).hexdigest()]
+            keys = sorted(fb.keys())
+            dims = {k: case["dim"] for k in keys
+                    if case["dim"] < len(fb.metadata(k).shape) and fb.metadata(k).shape[case["dim"]] >= world}
+            views = fb.get_tensors(keys, dims=dims) if batched else {
+                k: (fb.get_sharded(k, dims[k]) if k in dims else fb.get_tensor(k)) for k in keys}
+            for k in keys:
+                v = views[k]
+                got[k] = ["shard" if k in dims else "full", list(v.shape), hashlib.sha256(v.tobytes()).hexdigest()]
             fb.close()
             loader.close()
             out[(case["id"], auto)] = got == case["ranks"][rank]
@@ -114,6 +116,33 @@ def test_ipc_plane_matches_reference_loader(world):
 
 def golden_job_collective_plane(rank, world):
     return golden_job(rank, world, plane="nccl")
+
+
+def golden_job_collective_plane_batched(rank, world):
+    return golden_job(rank, world, plane="nccl", batched=True)
+
+
+def golden_job_ipc_batched(rank, world):
+    return golden_job(rank, world, plane="ipc", batched=True)
+
+
+def golden_job_collective_plane_batched_bcast(rank, world):
+    from paper_2505_23072_b200 import loader
+
+    loader.BIG_BROADCAST = 0  # every replicated tensor through the broadcast branch
+    return golden_job(rank, world, plane="nccl", batched=True)
+
+
+@pytest.mark.parametrize("job", ["collective", "collective_bcast", "ipc"])
+@pytest.mark.timeout(600)
+def test_batched_planes_match_reference_loader(job):
+    """get_tensors as ONE batch per case: the collective plane's single
+    owner-side launch + grouped point-to-point call, and the ipc plane's
+    single pull launch, against the reference loader's outputs."""
+    fn = {"collective": golden_job_collective_plane_batched, "ipc": golden_job_ipc_batched,
+          "collective_bcast": golden_job_collective_plane_batched_bcast}[job]
+    for rank_result in _run(3, fn):
+        assert rank_result and all(rank_result.values()), rank_result
 
 
 @pytest.mark.parametrize("world", [2, 3])
