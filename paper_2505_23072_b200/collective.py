@@ -460,28 +460,16 @@ class DistGroup:
         is already in ``out``); the others receive into ``out``. One grouped
         send/recv (ncclGroupStart/End under torch), so uneven remainder parts
         need no padding."""
-        dist = self._dist
         if self.world_size == 1:
             return
-        # gloo moves CUDA tensors in collectives but not point-to-point: stage
-        # through host memory there (NCCL sends device memory directly)
-        stage = self.backend == "gloo" and out.is_cuda
-        ops, landing = [], out
+        ops = []
         if rank == src:
             if parts is None or len(parts) != self.world_size:
                 raise SpecMismatch("scatter owner must provide one part per rank")
-            for r in range(self.world_size):
-                if r != src and parts[r].numel():
-                    ops.append(dist.P2POp(dist.isend, parts[r].cpu() if stage else parts[r], self._global(r),
-                                          group=self.pg))
+            ops = [("send", parts[r], r) for r in range(self.world_size) if r != src and parts[r].numel()]
         elif out.numel():
-            landing = torch.empty(out.shape, dtype=out.dtype) if stage else out
-            ops.append(dist.P2POp(dist.irecv, landing, self._global(src), group=self.pg))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        if landing is not out:
-            out.copy_(landing)
+            ops = [("recv", out, src)]
+        self.p2p(ops)
 
     def p2p(self, ops: list[tuple[str, torch.Tensor, int]]) -> None:
         """One grouped point-to-point call for a whole batch (ncclGroupStart /
