@@ -253,3 +253,36 @@ def auto_plane_job(rank, world):
 @pytest.mark.parametrize("world", [2, 4])
 def test_auto_plane_probes_ipc(world):
     assert [r["plane"] for r in _run(world, auto_plane_job)] == ["ipc"] * world
+
+
+def vllm_iter_job(rank, world):
+    """vllm_loader.weights_iterator under torch.distributed (vLLM's TP
+    workers): files spread over the ranks, every rank gets every tensor."""
+    import numpy as np
+
+    from paper_2505_23072_b200.format import DType, write_file
+    from paper_2505_23072_b200.vllm_loader import weights_iterator
+
+    d = f"/tmp/hl_vllm_iter_{os.getppid()}"
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(5)
+    tensors, files = {}, []
+    for i in range(3):
+        t = {f"m{i}.w": (DType.BF16, (64, 48), rng.integers(0, 256, 64 * 48 * 2, dtype=np.uint8).tobytes()),
+             f"m{i}.b": (DType.F32, (48,), rng.integers(0, 256, 48 * 4, dtype=np.uint8).tobytes())}
+        tensors.update(t)
+        p = f"{d}/model-{i + 1:05d}-of-00003.safetensors"
+        if rank == 0:
+            with open(p, "wb") as f:
+                f.write(write_file(t))
+        files.append(p)
+    torch.distributed.barrier()
+    got = {}
+    for name, t in weights_iterator(files):
+        got[name] = t.contiguous().view(torch.uint8).cpu().numpy().tobytes() == tensors[name][2]
+    return {"all_keys": set(got) == set(tensors), **got}
+
+
+def test_vllm_iterator_multirank():
+    for rank_result in _run(2, vllm_iter_job):
+        assert all(rank_result.values()), rank_result
