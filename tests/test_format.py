@@ -123,3 +123,28 @@ def test_stream_writer(tmp_path):
     assert h.body_offset % 8 == 0
     got = oracle.load_all([tmp_path / "s.safetensors"])
     assert got["a"][1] == data[0].tobytes() and got["b"][1] == data[1].tobytes()
+
+
+def test_reference_outcomes_on_fuzzed_headers():
+    """386 headers (valid layouts, every field corruption the reference checks,
+    random byte flips) give the SAME outcome as the reference's parse_header +
+    validate: the same error class, or the same parsed layout
+    (tests/golden/format_cases.json, made by the reference itself)."""
+    import base64
+
+    from paper_2505_23072_b200 import errors
+
+    cases = json.loads((GOLDEN / "format_cases.json").read_text())["cases"]
+    mismatches = []
+    for c in cases:
+        blob = base64.b64decode(c["blob"])
+        try:
+            h = parse_header(blob)
+            validate(h, c["file_size"])
+            got = {"body_offset": h.body_offset, "metadata": h.metadata,
+                   "tensors": [[m.name, m.dtype.value, list(m.shape), list(m.data_offsets)] for m in h.tensors.values()]}
+        except errors.AggloadError as e:
+            got = {"error": type(e).__name__}
+        if got != c["expect"]:
+            mismatches.append((c["tag"], c["expect"], got))
+    assert not mismatches, mismatches[:5]
