@@ -145,3 +145,25 @@ def test_bench_cpu_reference_leg(tmp_path, rng, world):
     r = bench.run_cpu_reference(paths, steps=1, warmup=0, world=world, policy=policy)
     assert r["kind"] == "port" and r["cores"] >= world
     assert f"{expect} ready tensor bytes" in r["sample"]
+
+
+def test_partition_matches_reference_outcomes():
+    """400 random shapes x dims (incl. out of range) x world sizes: same part
+    shapes, bounds and rejections as the reference's partition (golden made by
+    the reference, tests/golden/partition_cases.json)."""
+    import json
+    import math
+
+    from paper_2505_23072_b200 import errors
+
+    for c in json.loads((GOLDEN / "partition_cases.json").read_text())["cases"]:
+        shape = tuple(c["shape"])
+        n = math.prod(shape) if shape else 1
+        m = TensorMetadata("k", DType.BF16, shape, (0, 2 * n))
+        try:
+            spec = partition(m, c["dim"], c["world"])
+            got = {"part_shapes": [list(p) for p in spec.part_shapes],
+                   "bounds": [list(spec.bounds(r)) for r in range(c["world"])]}
+        except errors.AggloadError as e:
+            got = {"error": type(e).__name__}
+        assert got == c["expect"], c
