@@ -243,13 +243,20 @@ def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=Non
             t.join()
         owner = {k: ld for ld in loaders.values() for k in ld.index}
         got = [0] * world
+        # the reference's broadcast / scatter rendezvous twice per key (the data
+        # exchange and the "done" exchange, collective.py:175-255)
+        meet = threading.Barrier(world) if world > 1 else None
 
         def retrieve(r):
             nb = 0
             for k, ld in owner.items():
                 d = policy.get(k) if world > 1 else None
                 tag = cast.value if cast is not None else None
+                if meet:
+                    meet.wait()
                 nb += (ld.get_tensor(k, tag) if d is None else ld.get_sharded(k, d, world, r, tag)).nbytes
+                if meet:
+                    meet.wait()
             got[r] = nb
 
         ts = [threading.Thread(target=retrieve, args=(r,)) for r in range(world)]
@@ -267,7 +274,7 @@ def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=Non
     return {"value": ready / t / 1e9, "unit": "GB/s", "cores": threads, "kind": "port", "seconds": t,
             "sample": f"full workload: {len(paths)} file(s), {ready} ready tensor bytes over {world} rank(s), warm "
                       f"page cache; reference thread rule per rank ({sorted(set(workers.values()))} preadv "
-                      f"worker(s)), then {world} retrieval thread(s) (auto-release clones"
+                      f"worker(s)), then {world} retrieval thread(s) meeting twice per key (auto-release clones"
                       + (" / Megatron-dim slices" if world > 1 else "")
                       + (f", numpy {cast.value} conversion" if cast is not None else "")
                       + f"); host os.cpu_count()={os.cpu_count()}"}
