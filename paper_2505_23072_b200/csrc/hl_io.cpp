@@ -241,16 +241,23 @@ int ensure_ring_memory(hl_ctx* ctx, double* seconds) {
   bool registered = false;
   if (posix_memalign(&m, 2ull << 20, bytes) == 0) {
     madvise(m, bytes, MADV_HUGEPAGE);
-    std::thread toucher([&] {  // first touch on the GPU's NUMA node
-      if (!ctx->cpus.empty()) {
-        cpu_set_t set;
-        CPU_ZERO(&set);
-        for (int c : ctx->cpus) CPU_SET(c, &set);
-        sched_setaffinity(0, sizeof set, &set);
-      }
-      memset(m, 0, bytes);
-    });
-    toucher.join();
+    // first touch on the GPU's NUMA node, in parallel (page faults + zeroing dominate)
+    const uint64_t nt = std::max<uint64_t>(1, std::min<uint64_t>(ctx->cfg.workers, bytes >> 21));
+    const uint64_t piece = round_up((bytes + nt - 1) / nt, 2ull << 20);
+    std::vector<std::thread> touchers;
+    for (uint64_t i = 0; i < nt; ++i) {
+      touchers.emplace_back([&, i] {
+        if (!ctx->cpus.empty()) {
+          cpu_set_t set;
+          CPU_ZERO(&set);
+          for (int c : ctx->cpus) CPU_SET(c, &set);
+          sched_setaffinity(0, sizeof set, &set);
+        }
+        const uint64_t b = i * piece, e = std::min(bytes, b + piece);
+        if (b < e) memset((uint8_t*)m + b, 0, e - b);
+      });
+    }
+    for (auto& t : touchers) t.join();
     if (cudaHostRegister(m, bytes, cudaHostRegisterPortable) == cudaSuccess) {
       registered = true;
     } else {
