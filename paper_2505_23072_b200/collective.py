@@ -81,7 +81,7 @@ def _fresh(pool, name: str, dtype: DType, shape: tuple[int, ...]):
     for d in shape:
         n *= d
     nb = n * dtype.size_bytes
-    buf = pool.allocate(nb)
+    buf = pool.allocate(nb, carve=True)  # per-key outputs: carved from shared chunks
     return buf, make_view(buf, 0, TensorMetadata(name, dtype, tuple(shape), (0, nb)))
 
 

@@ -58,6 +58,7 @@ DIRECT_ALIGNMENT = 512               # ref device.py:51 (simdirect landing granu
 GDS_ALIGNMENT = 4096                 # cuFile / O_DIRECT block granularity
 DEFAULT_HOST_BOUNCE = 4 * 1024 * 1024  # pinned chunk per pread + H2D hop (ref: 160 MiB host bounce; 4 MiB measured best, profiles/)
 DEFAULT_ALIGN_BOUNCE = 16 * 1024 * 1024  # kept for API parity; the realign kernel needs no bounce
+CARVE_CHUNK = 1 << 30                # largest shared chunk per-key outputs are carved from
 
 
 class BackendKind(Enum):
@@ -196,8 +197,39 @@ class DevicePool:
         self.allocated_bytes = 0
         self.pooled_bytes = 0
         self.cumulative_pooled_bytes = 0
+        # carving: per-key outputs sliced from shared chunks (see _carve)
+        self._chunk: torch.Tensor | None = None
+        self._chunk_off = 0
+        self._expect = 0
 
-    def allocate(self, size: int, zero: bool = False) -> DeviceBuffer:
+    def expect(self, nbytes: int) -> None:
+        """Announce roughly how many bytes of per-key outputs are coming
+        (sizes the carving chunks)."""
+        with self._lock:
+            self._expect = max(0, int(nbytes))
+
+    def end_carving(self) -> None:
+        """Drop the pool's reference to the current chunk (slices keep theirs)."""
+        with self._lock:
+            self._chunk, self._chunk_off, self._expect = None, 0, 0
+
+    def _carve(self, nbytes: int) -> torch.Tensor:
+        """A 256-byte aligned slice of a shared chunk. A fresh process pays
+        one cudaMalloc per torch caching-allocator segment; carving the ~300
+        per-key outputs of a checkpoint out of a few chunks (each sized by the
+        announced remaining bytes, at most CARVE_CHUNK) turns a first load's
+        ~1 s of allocator growth into a few calls. Accounting stays per buffer;
+        a chunk's memory returns when its last slice dies."""
+        if self._chunk is None or self._chunk_off + nbytes > self._chunk.numel():
+            size = max(nbytes, min(CARVE_CHUNK, max(self._expect, nbytes)))
+            self._chunk = torch.empty(size, dtype=torch.uint8, device=self.device)
+            self._chunk_off = 0
+        t = self._chunk[self._chunk_off:self._chunk_off + nbytes]
+        self._chunk_off += (nbytes + 255) & ~255
+        self._expect = max(0, self._expect - nbytes)
+        return t
+
+    def allocate(self, size: int, zero: bool = False, carve: bool = False) -> DeviceBuffer:
         if size < 0:
             raise ValueError(f"allocation size must be non-negative, got {size}")
         with self._lock:
@@ -214,7 +246,14 @@ class DevicePool:
                             f"{self.allocated_bytes} live of {self.capacity_cap} cap")
             try:
                 # +16: 16-byte vector loads of a tensor's last bytes stay inside the allocation
-                t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)
+                if carve:
+                    try:
+                        t = self._carve(max(size, 1) + 16)
+                    except torch.OutOfMemoryError:
+                        self._chunk, self._chunk_off = None, 0
+                        t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)
+                else:
+                    t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)
             except torch.OutOfMemoryError as e:
                 raise OutOfMemory(f"device {self.device_id}: cannot allocate {size} bytes: {e}") from None
             if zero:
