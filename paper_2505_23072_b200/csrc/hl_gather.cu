@@ -583,24 +583,24 @@ struct DevInfo {
   int blocks_per_sm[5][kWhich] = {};
 };
 
-static const DevInfo& dev_info() {
+// Resident-grid cap of one kernel variant on the current device: SM count x
+// blocks per SM, queried the first time that variant launches (querying all
+// 20 variants up front would load every kernel of the module in a fresh
+// process — lazy module loading makes that a first-load cost).
+static uint64_t grid_cap(int kind, int which) {
   static std::mutex mu;
   static DevInfo cache[64];
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
   DevInfo& di = cache[dev & 63];
-  if (di.sms == 0) {
-    cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
-    for (int k = 0; k < 5; ++k) {
-      for (int w = 0; w < kWhich; ++w) {
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(k, w), kThreads, 0);
-        di.blocks_per_sm[k][w] = b > 0 ? b : 1;
-      }
-    }
+  if (di.sms == 0) cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+  if (di.blocks_per_sm[kind][which] == 0) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(kind, which), kThreads, 0);
+    di.blocks_per_sm[kind][which] = b > 0 ? b : 1;
   }
-  return di;
+  return (uint64_t)di.sms * di.blocks_per_sm[kind][which];
 }
 
 // Translate one ABI descriptor into kernel descriptors: the main one, plus an
@@ -673,9 +673,8 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
 
 static int launch(int kind, int which, Params& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
-  const DevInfo& di = dev_info();
   const uint64_t want = (p.total_units + kWarps - 1) / kWarps;
-  const uint64_t cap = (uint64_t)di.sms * di.blocks_per_sm[kind][which];
+  const uint64_t cap = grid_cap(kind, which);
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   if (p.n <= (uint32_t)kSmallDescs) {
     SmallParams sp;
