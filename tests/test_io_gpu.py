@@ -95,7 +95,7 @@ def test_forced_cufile_compat_mode_in_subprocess(blob, tmp_path):
         "print('EQUAL', ok)\n" % (str(ROOT), 4 << 20, str(path), 4 << 20, str(path), 4 << 20))
     env = dict(os.environ, HL_FORCE_CUFILE="1")
     try:
-        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=90)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=30)
     except subprocess.TimeoutExpired:
         pytest.xfail("cuFile compat mode (no nvidia-fs) hangs in cuFileRead on this host")
     if r.returncode != 0:
