@@ -422,3 +422,29 @@ def test_upstream_spellings_as_dict_filename_shape(tmp_path, rng):
     for k in req:
         assert got[k].tobytes() == t[k][2]  # world 1: every shard is the full tensor
     fb.close()
+
+
+def test_safe_open_and_context_managers(tmp_path, rng):
+    """safetensors/fastsafe_open-style convenience and `with` on the loader
+    and the handle (superset API)."""
+    from paper_2505_23072_b200 import safe_open
+
+    t = random_tensor_set(rng, 5, prefix="o", dtypes=[DType.BF16, DType.F32, DType.I64])
+    p = _write(tmp_path, "o.safetensors", t)
+    with safe_open(str(p), device="cuda:0") as f:
+        assert sorted(f.keys()) == sorted(t)
+        for k, (dt, shape, raw) in t.items():
+            x = f.get_tensor(k)
+            assert x.is_cuda and tuple(x.shape) == shape
+            assert x.reshape(-1).view(torch.uint8).cpu().numpy().tobytes() == raw
+    with SafeTensorsFileLoader(SingleGroup(), "host") as loader:
+        loader.add_filenames({0: [p]})
+        with loader.copy_files_to_device() as fb:
+            v = fb.get_tensor(sorted(t)[0])
+            x = v.torch
+        with pytest.raises(UseAfterClose):
+            fb.get_tensor(sorted(t)[1])
+        with pytest.raises(UseAfterClose):  # the reference's close invalidates returned handles
+            v.tobytes()
+    # ... while the torch tensor the user holds stays valid (torch owns the memory)
+    assert x.reshape(-1).view(torch.uint8).cpu().numpy().tobytes() == t[sorted(t)[0]][2]
