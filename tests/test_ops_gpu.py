@@ -1,0 +1,83 @@
+"""API-semantics parity: random op sequences (get_tensor / get_sharded on
+live, repeated, dropped and stale keys, unknown keys, bad dims, close, reads
+after close) replayed on the B200 loader must give exactly the outcomes the
+REFERENCE loader gave — same bytes (sha256) and shapes, or the same error
+class — on every rank (tests/golden/ops_cases.json, made by the reference:
+tests/golden/make_ops_golden.py). Thread ranks share the one GPU."""
+
+from __future__ import annotations
+
+import gc
+import hashlib
+import json
+import threading
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN  # noqa: E402
+from paper_2505_23072_b200 import LoaderConfig, ProcessGroup, SafeTensorsFileLoader  # noqa: E402
+from paper_2505_23072_b200.transfer import NumaNode, Topology  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CASES = json.loads((GOLDEN / "ops_cases.json").read_text())["cases"]
+
+
+def replay(case):
+    files = [GOLDEN / "corpora" / f for f in case["files"]]
+    world = case["world"]
+    mapping = {r: [str(p) for i, p in enumerate(files) if i % world == r] for r in range(world)}
+    topo = Topology((NumaNode(0, 32, tuple(range(world)), (0,)),))
+    group = ProcessGroup(world, timeout=60)
+    out, errors = [None] * world, {}
+
+    def rank_main(rank):
+        try:
+            ld = SafeTensorsFileLoader(group, rank=rank, config=LoaderConfig(
+                backend=case["backend"], topology=topo, auto_release=case["auto_release"]))
+            ld.add_filenames(mapping)
+            fb = ld.copy_files_to_device()
+            held, trace = {}, []
+            for i, op in enumerate(case["ops"]):
+                try:
+                    if op[0] in ("tensor", "shard"):
+                        v = fb.get_tensor(op[1]) if op[0] == "tensor" else fb.get_sharded(op[1], op[2])
+                        held[i] = v
+                        trace.append(["ok", list(v.shape), hashlib.sha256(v.tobytes()).hexdigest()])
+                    elif op[0] == "drop":
+                        held.pop(op[1], None)
+                        gc.collect()
+                        trace.append(["ok"])
+                    elif op[0] == "read":
+                        v = held.get(op[1])
+                        trace.append(["ok", hashlib.sha256(v.tobytes()).hexdigest()] if v is not None else ["ok"])
+                    elif op[0] == "close":
+                        fb.close()
+                        trace.append(["ok"])
+                except Exception as e:  # noqa: BLE001 - the class name is the outcome
+                    trace.append(["err", type(e).__name__])
+            out[rank] = trace
+            fb.close()
+            ld.close()
+        except BaseException as e:  # noqa: BLE001
+            errors[rank] = e
+
+    ts = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(300)
+    assert not errors, errors
+    return out
+
+
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_op_sequence_matches_reference(i):
+    case = CASES[i]
+    got = replay(case)
+    for rank in range(case["world"]):
+        for j, (g, e) in enumerate(zip(got[rank], case["ranks"][rank])):
+            assert g == e, (f"rank {rank} op {j} {case['ops'][j]}: got {g}, reference {e}", case["backend"],
+                            case["auto_release"], case["world"])
