@@ -286,3 +286,69 @@ def vllm_iter_job(rank, world):
 def test_vllm_iterator_multirank():
     for rank_result in _run(2, vllm_iter_job):
         assert all(rank_result.values()), rank_result
+
+
+def ops_job(rank, world, plane):
+    """Replay every reference op trace of this world size (tests/golden/ops_cases.json)
+    through DistGroup on the given data plane; outcomes must equal the reference's."""
+    import gc
+    import json
+
+    from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader
+    from paper_2505_23072_b200.transfer import NumaNode, Topology
+
+    group = DistGroup(device=torch.device("cuda", 0), data_plane=plane)
+    result = {}
+    for ci, case in enumerate(json.loads((GOLDEN / "ops_cases.json").read_text())["cases"]):
+        if case["world"] != world:
+            continue
+        files = [GOLDEN / "corpora" / f for f in case["files"]]
+        mapping = {r: [str(p) for i, p in enumerate(files) if i % world == r] for r in range(world)}
+        topo = Topology((NumaNode(0, 32, tuple(range(world)), (0,)),))
+        ld = SafeTensorsFileLoader(group, config=LoaderConfig(backend=case["backend"], topology=topo,
+                                                              auto_release=case["auto_release"]))
+        ld.add_filenames(mapping)
+        fb = ld.copy_files_to_device()
+        held, trace = {}, []
+        for i, op in enumerate(case["ops"]):
+            try:
+                if op[0] in ("tensor", "shard"):
+                    v = fb.get_tensor(op[1]) if op[0] == "tensor" else fb.get_sharded(op[1], op[2])
+                    held[i] = v
+                    trace.append(["ok", list(v.shape), hashlib.sha256(v.tobytes()).hexdigest()])
+                elif op[0] == "drop":
+                    held.pop(op[1], None)
+                    gc.collect()
+                    trace.append(["ok"])
+                elif op[0] == "read":
+                    v = held.get(op[1])
+                    trace.append(["ok", hashlib.sha256(v.tobytes()).hexdigest()] if v is not None else ["ok"])
+                elif op[0] == "close":
+                    fb.close()
+                    trace.append(["ok"])
+            except Exception as e:  # noqa: BLE001
+                trace.append(["err", type(e).__name__])
+        fb.close()
+        ld.close()
+        exp = case["ranks"][rank]
+        bad = [(j, case["ops"][j], g, e) for j, (g, e) in enumerate(zip(trace, exp)) if g != e]
+        result[ci] = True if not bad else str(bad[0])
+    return result
+
+
+def ops_job_ipc(rank, world):
+    return ops_job(rank, world, "ipc")
+
+
+def ops_job_collective(rank, world):
+    return ops_job(rank, world, "nccl")
+
+
+@pytest.mark.parametrize("plane", ["ipc", "collective"])
+@pytest.mark.timeout(900)
+def test_planes_replay_reference_op_traces(plane):
+    fn = ops_job_ipc if plane == "ipc" else ops_job_collective
+    for world in (2, 3):
+        for rank_result in _run(world, fn, timeout=600):
+            bad = {k: v for k, v in rank_result.items() if v is not True}
+            assert rank_result and not bad, (world, bad)
