@@ -288,14 +288,15 @@ def test_vllm_iterator_multirank():
         assert all(rank_result.values()), rank_result
 
 
-def ops_job(rank, world, plane):
+def ops_job(rank, world, plane, batched=False):
     """Replay every reference op trace of this world size (tests/golden/ops_cases.json)
-    through DistGroup on the given data plane; outcomes must equal the reference's."""
-    import gc
+    through DistGroup on the given data plane; outcomes must equal the reference's.
+    batched: runs of fresh keys go through one get_tensors call."""
     import json
 
     from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader
     from paper_2505_23072_b200.transfer import NumaNode, Topology
+    from test_ops_gpu import runs_of, step
 
     group = DistGroup(device=torch.device("cuda", 0), data_plane=plane)
     result = {}
@@ -310,24 +311,10 @@ def ops_job(rank, world, plane):
         ld.add_filenames(mapping)
         fb = ld.copy_files_to_device()
         held, trace = {}, []
-        for i, op in enumerate(case["ops"]):
-            try:
-                if op[0] in ("tensor", "shard"):
-                    v = fb.get_tensor(op[1]) if op[0] == "tensor" else fb.get_sharded(op[1], op[2])
-                    held[i] = v
-                    trace.append(["ok", list(v.shape), hashlib.sha256(v.tobytes()).hexdigest()])
-                elif op[0] == "drop":
-                    held.pop(op[1], None)
-                    gc.collect()
-                    trace.append(["ok"])
-                elif op[0] == "read":
-                    v = held.get(op[1])
-                    trace.append(["ok", hashlib.sha256(v.tobytes()).hexdigest()] if v is not None else ["ok"])
-                elif op[0] == "close":
-                    fb.close()
-                    trace.append(["ok"])
-            except Exception as e:  # noqa: BLE001
-                trace.append(["err", type(e).__name__])
+        runs = runs_of(case, 0) if batched else {}
+        i = 0
+        while i < len(case["ops"]):
+            i = step(fb, case["ops"], i, held, trace, runs)
         fb.close()
         ld.close()
         exp = case["ranks"][rank]
@@ -344,10 +331,19 @@ def ops_job_collective(rank, world):
     return ops_job(rank, world, "nccl")
 
 
-@pytest.mark.parametrize("plane", ["ipc", "collective"])
+def ops_job_ipc_batched(rank, world):
+    return ops_job(rank, world, "ipc", batched=True)
+
+
+def ops_job_collective_batched(rank, world):
+    return ops_job(rank, world, "nccl", batched=True)
+
+
+@pytest.mark.parametrize("plane", ["ipc", "collective", "ipc_batched", "collective_batched"])
 @pytest.mark.timeout(900)
 def test_planes_replay_reference_op_traces(plane):
-    fn = ops_job_ipc if plane == "ipc" else ops_job_collective
+    fn = {"ipc": ops_job_ipc, "collective": ops_job_collective, "ipc_batched": ops_job_ipc_batched,
+          "collective_batched": ops_job_collective_batched}[plane]
     for world in (2, 3):
         for rank_result in _run(world, fn, timeout=600):
             bad = {k: v for k, v in rank_result.items() if v is not True}
