@@ -112,10 +112,10 @@ def main():
     corpora = json.loads((HERE / "corpora" / "expect.json").read_text())["cases"]
     rng = np.random.default_rng(0x0B5)
     cases = []
-    for ci in range(36):
+    for ci in range(100):
         c = corpora[int(rng.integers(0, len(corpora)))]
         files = [HERE / "corpora" / f for f in c["files"]]
-        world = int(rng.integers(1, 4))
+        world = int(rng.integers(1, 5))
         backend = ["host", "simdirect"][int(rng.integers(0, 2))]
         auto = bool(rng.integers(0, 2))
         shapes = {}
@@ -123,7 +123,7 @@ def main():
             for k, m in read_header(p).tensors.items():
                 shapes[k] = tuple(m.shape)
         keys = sorted(shapes)
-        ops = make_ops(rng, keys, shapes, int(rng.integers(8, 30)))
+        ops = make_ops(rng, keys, shapes, int(rng.integers(8, 50)))
         traces = run(files, world, backend, auto, ops)
         if any(t is None for t in traces):
             continue  # a rank hung (never expected); skip rather than record garbage

@@ -344,7 +344,7 @@ def ops_job_collective_batched(rank, world):
 def test_planes_replay_reference_op_traces(plane):
     fn = {"ipc": ops_job_ipc, "collective": ops_job_collective, "ipc_batched": ops_job_ipc_batched,
           "collective_batched": ops_job_collective_batched}[plane]
-    for world in (2, 3):
+    for world in (2, 3, 4):
         for rank_result in _run(world, fn, timeout=600):
             bad = {k: v for k, v in rank_result.items() if v is not True}
             assert rank_result and not bad, (world, bad)

@@ -101,8 +101,10 @@ def replay(case, batched=False):
             out[rank] = trace
             fb.close()
             ld.close()
-        except BaseException as e:  # noqa: BLE001
-            errors[rank] = e
+        except BaseException:  # noqa: BLE001
+            import traceback
+
+            errors[rank] = traceback.format_exc()
 
     ts = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
     for t in ts:
