@@ -93,8 +93,19 @@ def ensure_data(arch: str, data_dir: str, header: str, rank: int, world: int, di
     d = Path(data_dir) / tag
     marker = d / "READY"
     if rank == 0 and not marker.exists():
+        import shutil
+
         import torch
 
+        need = int(sum(synth.nbytes(e) for e in ents) * 1.05) + (1 << 30)
+        Path(data_dir).mkdir(parents=True, exist_ok=True)
+        if shutil.disk_usage(data_dir).free < need:
+            # make room: drop OUR other generated checkpoints (READY-marked dirs next to this one)
+            for other in sorted(Path(data_dir).iterdir()):
+                if other != d and (other / "READY").exists():
+                    shutil.rmtree(other, ignore_errors=True)
+                    if shutil.disk_usage(data_dir).free >= need:
+                        break
         t0 = time.time()
         synth.generate(arch, d, header=header, seed=0, device="cuda" if torch.cuda.is_available() else None,
                        max_bytes=max_bytes, layers=layers)

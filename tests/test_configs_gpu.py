@@ -39,6 +39,17 @@ pytestmark = pytest.mark.gpu
 DATA = Path(os.environ.get("HL_TEST_DATA", tempfile.gettempdir())) / "hl_configs"
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _free_disk_after_module():
+    """The config corpora take ~35 GB: remove them when the module is done
+    (the box's disk is shared with bench.py's data); HL_KEEP_TEST_DATA=1 keeps them."""
+    yield
+    if os.environ.get("HL_KEEP_TEST_DATA") != "1":
+        import shutil
+
+        shutil.rmtree(DATA, ignore_errors=True)
+
+
 def _gen(name, arch, header="aligned", layers=None, max_bytes=None):
     d = DATA / name
     if not (d / "READY").exists():
