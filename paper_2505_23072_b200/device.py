@@ -25,6 +25,8 @@ moves after landing (realign, clone, shard pack, cast) are ``hl_gather``.
 
 from __future__ import annotations
 
+import math
+import os
 import threading
 import weakref
 from dataclasses import dataclass
@@ -34,13 +36,16 @@ import torch
 
 from . import _native
 from .errors import (
+    BounceTooSmall,
     DoubleRelease,
+    IoError,
+    MisalignedDirectTransfer,
     NativeUnavailable,
     OutOfBoundsView,
     OutOfMemory,
     UnsupportedConversion,
 )
-from .format import DType
+from .format import DType, TensorMetadata
 
 __all__ = [
     "BackendKind",
@@ -52,6 +57,10 @@ __all__ = [
     "DEFAULT_ALIGN_BOUNCE",
     "cuda_device",
     "conversion_supported",
+    "transfer_from_file",
+    "align_and_convert",
+    "align_fix",
+    "convert_dtype",
 ]
 
 DIRECT_ALIGNMENT = 512               # ref device.py:51 (simdirect landing granularity)
@@ -284,3 +293,140 @@ class DevicePool:
                 self.pooled_bytes += buf.capacity
                 self.cumulative_pooled_bytes += buf.capacity
             buf._tensor = None  # torch's caching allocator takes it back once views die
+
+
+# ---------------------------------------------------------------- device sub-boundary
+# The reference's device backend also exposes its building blocks one call at a
+# time (ref device.py:238-590): a ranged file -> device transfer, the realign
+# repack, and an in-place dtype conversion. The loader never calls these (it
+# lands whole files through the engine and realigns out of place in one batched
+# launch, loader.py _land); they exist so code written against the reference's
+# device module keeps working, with the same arguments, results and errors, on
+# the same engine and kernel as the hot path.
+
+def _path_of(file) -> str:
+    """A readable path for the engine: an fd or file object (the reference's
+    ``_fd_of`` inputs, ref device.py:220-223) resolves through /proc."""
+    if isinstance(file, (str, bytes)) or hasattr(file, "__fspath__"):
+        return os.fsdecode(file)
+    fd = file if isinstance(file, int) else file.fileno()
+    return os.readlink(f"/proc/self/fd/{fd}")
+
+
+def transfer_from_file(buf: DeviceBuffer, dev_off: int, file, file_off: int, length: int,
+                       staging=None) -> None:
+    """Copy ``length`` file bytes at ``file_off`` into ``buf`` at ``dev_off``
+    (ref device.py:238-288): bounds, the direct backends' alignment rule (offsets
+    and length multiples of the landing granularity unless the range ends at
+    end-of-file: MisalignedDirectTransfer), IoError on a short file. The bytes
+    move through the native engine's pinned ring (``hl_transfer_from_file``);
+    ``staging`` is accepted for signature parity — the ring is the staging — and
+    a zero-capacity one raises BounceTooSmall as in the reference."""
+    from .transfer import engine_for, engine_team  # transfer imports this module
+
+    buf._check_range(dev_off, length)
+    path = _path_of(file)
+    if length == 0:
+        return
+    kind = buf.backend.kind
+    if kind is not BackendKind.HOST:
+        align = buf.backend.transfer_alignment
+        if file_off % align or dev_off % align:
+            raise MisalignedDirectTransfer(f"direct transfer needs {align}-byte aligned offsets, "
+                                           f"got file_off={file_off} dev_off={dev_off}")
+        if length % align and file_off + length != os.stat(path).st_size:
+            raise MisalignedDirectTransfer(f"direct transfer length {length} is not a {align} multiple "
+                                           "and does not end at end-of-file")
+    elif staging is not None and min(buf.backend.bounce_buffer_bytes, getattr(staging, "nbytes", len(staging))) <= 0:
+        raise BounceTooSmall("host staging buffer has zero capacity")
+    if file_off + length > os.stat(path).st_size:
+        raise IoError(f"unexpected EOF: [{file_off}, {file_off + length}) past the end of {path}")
+    eng = engine_for(buf.device_id, engine_team(), buf.backend.bounce_buffer_bytes, buf.backend.io_mode)
+    with torch.cuda.device(buf.device_id):
+        eng.transfer(path, file_off, length, buf.ptr + dev_off)
+
+
+def _scratch_rewrite(buf: DeviceBuffer, end: int, descs_into) -> None:
+    """Rewrite ``buf[0:end)`` in place without the reference's overlap-ordered
+    chunk moves: snapshot the region, let ``descs_into(scratch_ptr)`` build the
+    moves from the ORIGINAL bytes into the snapshot, copy it back. Bytes no move
+    writes (alignment padding, a narrowed tail) keep their old values, exactly as
+    the reference's in-place moves leave them. Three hl_gather launches on the
+    current stream."""
+    from . import kernels  # kernels is a leaf module; imported lazily to keep this one light
+
+    dev = torch.device("cuda", buf.device_id)
+    scratch = torch.empty(max(end, 1), dtype=torch.uint8, device=dev)
+    kernels.run([kernels.copy_desc(buf.ptr, scratch.data_ptr(), end, DType.U8)], dev)
+    kernels.run(descs_into(scratch.data_ptr()), dev)
+    kernels.run([kernels.copy_desc(scratch.data_ptr(), buf.ptr, end, DType.U8)], dev)
+
+
+def align_and_convert(buf: DeviceBuffer, landing, bounce: int, conversions: dict | None = None) -> list:
+    """Repack tensors to dtype-aligned offsets, converting dtypes in the same
+    pass (ref device.py:466-534): ascending landing order, each start rounded up
+    to the (target) dtype's alignment; a no-op returning the landing offsets
+    when nothing converts and everything is aligned. Errors as the reference:
+    UnsupportedConversion, OutOfBoundsView when the repacked layout outgrows the
+    buffer, BounceTooSmall when ``bounce`` cannot hold one element (the kernel
+    needs no bounce; the check keeps the contract). Returns
+    ``[(name, new_offset, TensorMetadata)]``."""
+    from . import kernels
+
+    conversions = conversions or {}
+    entries = sorted(landing, key=lambda e: e[1])
+    for name, _, meta in entries:
+        target = conversions.get(name, meta.dtype)
+        if target is not meta.dtype:
+            check_conversion(meta.dtype, target, name)
+    if not conversions and all(off % meta.dtype.alignment == 0 for _, off, meta in entries):
+        return [(name, off, TensorMetadata(meta.name, meta.dtype, meta.shape, (off, off + meta.nbytes)))
+                for name, off, meta in entries]
+    moves, cursor = [], 0
+    for name, off, meta in entries:
+        buf._check_range(off, meta.nbytes)
+        dst = conversions.get(name, meta.dtype)
+        numel = math.prod(meta.shape)
+        dst_off = -(-cursor // dst.alignment) * dst.alignment
+        moves.append((name, off, dst_off, numel, meta, dst))
+        cursor = dst_off + numel * dst.size_bytes
+    if cursor > buf.capacity:
+        raise OutOfBoundsView(f"repacked layout needs {cursor} bytes but buffer capacity is {buf.capacity}")
+    max_elem = max((max(m[4].dtype.size_bytes, m[5].size_bytes) for m in moves), default=1)
+    if bounce < max_elem:
+        raise BounceTooSmall(f"bounce of {bounce} bytes cannot hold a {max_elem}-byte element")
+    src = buf.ptr
+    _scratch_rewrite(buf, cursor, lambda out: [
+        kernels.copy_desc(src + off, out + dst_off, numel, meta.dtype, dst)
+        for _, off, dst_off, numel, meta, dst in moves])
+    return [(name, dst_off, TensorMetadata(meta.name, dst, meta.shape, (dst_off, dst_off + numel * dst.size_bytes)))
+            for name, _, dst_off, numel, meta, dst in moves]
+
+
+def align_fix(buf: DeviceBuffer, landing, bounce: int = DEFAULT_ALIGN_BOUNCE) -> list:
+    """Repack so every offset is dtype-aligned; idempotent (ref device.py:537-548)."""
+    return [(name, off) for name, off, _ in align_and_convert(buf, landing, bounce)]
+
+
+def convert_dtype(buf: DeviceBuffer, view_meta: TensorMetadata, target: DType,
+                  bounce: int = DEFAULT_ALIGN_BOUNCE) -> TensorMetadata:
+    """Convert one tensor region in place, keeping its begin offset
+    (ref device.py:551-590); same checks and error classes as the reference."""
+    from . import kernels
+
+    check_conversion(view_meta.dtype, target)
+    numel = math.prod(view_meta.shape)
+    begin = view_meta.begin
+    dst_bytes = numel * target.size_bytes
+    if begin % target.alignment:
+        raise OutOfBoundsView(f"offset {begin} is not aligned for {target.value}")
+    if begin + dst_bytes > buf.capacity:
+        raise OutOfBoundsView(f"converted tensor needs [{begin}, {begin + dst_bytes}) but capacity is {buf.capacity}")
+    if bounce < max(view_meta.dtype.size_bytes, target.size_bytes):
+        raise BounceTooSmall(f"bounce of {bounce} bytes cannot hold one element")
+    if begin < 0 or begin + view_meta.nbytes > buf.capacity:
+        raise OutOfBoundsView(f"tensor [{begin}, {begin + view_meta.nbytes}) outside capacity {buf.capacity}")
+    src = buf.ptr + begin
+    end = max(begin + dst_bytes, begin + view_meta.nbytes)
+    _scratch_rewrite(buf, end, lambda out: [kernels.copy_desc(src, out + begin, numel, view_meta.dtype, target)])
+    return TensorMetadata(view_meta.name, target, view_meta.shape, (begin, begin + dst_bytes))

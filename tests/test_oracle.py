@@ -11,6 +11,7 @@
 from __future__ import annotations
 
 import hashlib
+import math
 import struct
 
 import numpy as np
@@ -122,6 +123,27 @@ def test_repack_layout_matches_reference_align_fix(golden_cases):
             aligned = all(off % oracle.SIZES[dt] == 0 for _, off, dt, _ in landing)
             exp = {k: off for k, off, _, _ in landing} if aligned else oracle.repack_layout(landing)
             assert exp == offs, (case["id"], f)
+
+
+def test_in_place_repack_matches_reference_whole_buffer():
+    """The oracle's align_and_convert restatement reproduces the reference's
+    whole buffer (sha256) and table on every successful device_cases.json case
+    (tests/golden/make_device_golden.py ran the reference itself)."""
+    import base64
+    import json
+
+    from conftest import GOLDEN
+
+    n = 0
+    for c in json.loads((GOLDEN / "device_cases.json").read_text())["cases"]:
+        if c["op"] != "align_and_convert" or "error" in c["expect"]:
+            continue
+        landing = [(k, off, dt, math.prod(shape)) for k, off, dt, shape in c["landing"]]
+        table, out = oracle.align_and_convert_bytes(base64.b64decode(c["input"]), landing, c["conversions"])
+        assert [[k, o, dt] for k, o, dt in table] == [t[:3] for t in c["expect"]["table"]], c
+        assert hashlib.sha256(out).hexdigest() == c["expect"]["sha256"], c
+        n += 1
+    assert n > 100
 
 
 def test_cpu_loader_port_round_trip(tmp_path, rng):
