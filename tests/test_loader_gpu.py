@@ -151,6 +151,49 @@ def test_order_mismatch_times_out(two_files):
     assert isinstance(err.value.exc, RendezvousTimeout)
 
 
+def test_any_identical_permutation_succeeds(tmp_path, rng):
+    """ref tests/test_loader.py:170-192: any key order works if every rank uses it."""
+    files = {}
+    for i in range(2):
+        tensors = random_tensor_set(rng, 3, prefix=f"f{i}_")
+        files[str(_write(tmp_path, f"f{i}.safetensors", tensors))] = tensors
+    mapping = {0: [sorted(files)[0]], 1: [sorted(files)[1]]}
+    expect = {k: raw for t in files.values() for k, (_, _, raw) in t.items()}
+    group = ProcessGroup(2)
+
+    for order in (list(rng.permutation(list(expect))) for _ in range(3)):
+        def rank_main(rank, order=order):
+            loader = SafeTensorsFileLoader(group, "host", rank=rank)
+            loader.add_filenames(mapping)
+            fb = loader.copy_files_to_device()
+            got = {k: fb.get_tensor(k).tobytes() for k in order}
+            fb.close()
+            return got
+
+        for got in run_ranks(2, rank_main):
+            assert got == expect
+
+
+def test_multirank_repeat_from_survivor(two_files):
+    """ref tests/test_loader.py:312-327: a consumed key whose owner buffer was
+    released is served again from the surviving view on every rank."""
+    pa, pb, a, _ = two_files
+    group = ProcessGroup(2)
+
+    def rank_main(rank):
+        loader = SafeTensorsFileLoader(group, "host", rank=rank)
+        loader.add_filenames({0: [str(pa)], 1: [str(pb)]})
+        fb = loader.copy_files_to_device()
+        first = fb.get_tensor("a0")
+        again = fb.get_tensor("a0")
+        out = first.tobytes(), again.tobytes()
+        fb.close()
+        return out
+
+    for first, again in run_ranks(2, rank_main):
+        assert first == again == a["a0"][2]
+
+
 def test_unknown_key_keeps_group_usable(two_files):
     pa, pb, *_ = two_files
     group = ProcessGroup(2)
