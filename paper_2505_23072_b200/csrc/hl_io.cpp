@@ -299,6 +299,8 @@ int ensure_slot(hl_ctx* ctx, uint32_t w, uint32_t k, Slot& s) {
   return HL_OK;
 }
 
+static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring);
+
 void worker_main(PlanRun* run, uint32_t w) {
   hl_ctx* ctx = run->ctx;
   cudaSetDevice(ctx->cfg.device);
@@ -321,6 +323,25 @@ void worker_main(PlanRun* run, uint32_t w) {
       return;
     }
   }
+  worker_loop(run, w, ring);
+  // Drain on every exit, failed or not: the caller frees (or reuses) the
+  // destination buffers as soon as hl_execute_plan returns, so no DMA of this
+  // worker may still be in flight, and no page-cache range may stay pinned.
+  cudaError_t e = cudaStreamSynchronize(ring.stream);
+  for (auto& s : ring.slots) {
+    s.busy = false;
+    if (s.reg) {
+      cudaHostUnregister(s.reg);
+      s.reg = nullptr;
+    }
+  }
+  if (e != cudaSuccess) run->fail(HL_ECUDA, std::string("H2D stream: ") + cudaGetErrorString(e));
+}
+
+// One worker's share of a plan: claim chunks, read, submit their H2D copies.
+// Returns on the first error (recorded in `run`); worker_main drains.
+static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
+  hl_ctx* ctx = run->ctx;
   const auto& chunks = *run->chunks;
   auto& files = *run->files;
   std::vector<unsigned char> vec;  // mincore scratch
@@ -458,15 +479,6 @@ void worker_main(PlanRun* run, uint32_t w) {
     }
     s.busy = true;
   }
-  cudaError_t e = cudaStreamSynchronize(ring.stream);
-  for (auto& s : ring.slots) {
-    s.busy = false;
-    if (s.reg) {
-      cudaHostUnregister(s.reg);
-      s.reg = nullptr;
-    }
-  }
-  if (e != cudaSuccess) run->fail(HL_ECUDA, std::string("H2D stream: ") + cudaGetErrorString(e));
 }
 
 double residency(int fd, uint64_t size) {
