@@ -729,8 +729,9 @@ def main():
     if rank == 0:
         roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
-                    "traffic": traffic, "kernel": "hl_gather row_kernel<"
-                    + (f"{src_dt.value}->{cast.value}" if cast else "K_COPY1") + ", aligned>",
+                    "traffic": traffic,
+                    "kernel": (f"hl_gather row_kernel<{src_dt.value}->{cast.value}, aligned>" if cast
+                               else "hl_gather bulk_kernel (TMA cp.async.bulk copy)"),
                     "launches_per_step": k_n, "algorithmic_bytes_per_launch": dom_bytes,
                     "achieved_all_launches_of_step": round(achieved_all, 1) if achieved_all else None,
                     # live: the kernel's share of the value step (the rest is host pre-launch work);

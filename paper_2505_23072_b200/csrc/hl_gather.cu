@@ -541,6 +541,87 @@ __global__ void __launch_bounds__(kThreads) generic_kernel(const __grid_constant
   }
 }
 
+// ---------------------------------------------------------------- TMA bulk copy
+// Aligned raw copies (clones, dim-0 shards, aligned rows of column shards: the
+// value leg's whole workload) need no register work at all, so they bypass the
+// SM's load/store pipes: one elected thread per CTA streams 16 KiB row chunks
+// HBM -> shared memory with cp.async.bulk (TMA, completion counted on an
+// mbarrier) and shared -> HBM with bulk_group stores, kBulkStages chunks in
+// flight. Measured on a flat 7.25 GB copy (tools/bulk_copy_probe.cu,
+// profiles/r01_bulk_copy_probe.jsonl): 6.51 TB/s vs 6.25 TB/s for the 16-byte
+// LDG/STG loop at this kernel's 4 resident blocks per SM.
+constexpr uint32_t kBulkChunk = 16u << 10;
+constexpr uint64_t kBulkVecs = kBulkChunk / 16;
+constexpr int kBulkStages = 4;
+constexpr int kBulkLag = 1;  // stores allowed to be still reading shared memory when a stage is refilled
+constexpr size_t kBulkSmem = (size_t)kBulkStages * kBulkChunk;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Unit u of a bulk launch: descriptors are single contiguous rows, so unit lu of
+// descriptor d is bytes [lu * kBulkChunk, ...) of it. Each stream of units
+// (loads, stores) visits increasing u, so its descriptor index only walks forward.
+template <class P>
+__device__ __forceinline__ void bulk_unit(const P& p, uint64_t u, uint32_t& di, const uint8_t*& src, uint8_t*& dst,
+                                          uint32_t& bytes) {
+  while (di + 1 < p.n && p.d[di + 1].unit_begin <= u) ++di;
+  const KDesc& d = p.d[di];
+  const uint64_t off = (u - d.unit_begin) * kBulkChunk;
+  const uint64_t total = d.row_len * 16;
+  src = reinterpret_cast<const uint8_t*>(d.src) + off;
+  dst = reinterpret_cast<uint8_t*>(d.dst) + off;
+  bytes = (uint32_t)min((uint64_t)kBulkChunk, total - off);
+}
+
+template <class P>
+__global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bar[kBulkStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kBulkStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint64_t policy;  // streaming: neither side is re-read by this launch
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
+  uint32_t load_hint = 0, store_hint = 0;
+  auto load = [&](uint64_t k) {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    bulk_unit(p, first + k * step, load_hint, src, dst, bytes);
+    const int s = (int)(k % kBulkStages);
+    const uint32_t b = smem_u32(&bar[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        :: "r"(smem_u32(stage + (size_t)s * kBulkChunk)), "l"(src), "r"(bytes), "r"(b), "l"(policy) : "memory");
+  };
+  constexpr uint64_t ahead = kBulkStages - kBulkLag;
+  for (uint64_t k = 0; k < mine && k < ahead; ++k) load(k);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    bulk_unit(p, first + k * step, store_hint, src, dst, bytes);
+    const int s = (int)(k % kBulkStages);
+    asm volatile(
+        "{\n .reg .pred ready;\n"
+        "WAIT: mbarrier.try_wait.parity.shared::cta.b64 ready, [%0], %1;\n"
+        " @!ready bra WAIT;\n}\n" :: "r"(smem_u32(&bar[s])), "r"((uint32_t)((k / kBulkStages) & 1)) : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 :: "l"(dst), "r"(smem_u32(stage + (size_t)s * kBulkChunk)), "r"(bytes), "l"(policy) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (k + ahead < mine) {
+      // the refilled stage was last read by store k - kBulkLag
+      asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(kBulkLag) : "memory");
+      load(k + ahead);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- host side
 static const uint32_t kSize[13] = {1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8};
 
@@ -566,8 +647,16 @@ static auto kernel_for(int which) -> void (*)(P) {
     default: return row_kernel<K, P, R_MIXED>;
   }
 }
+// Contiguous aligned raw copies (whole tensors, dim-0 shards) run on the TMA
+// bulk kernel (32 threads, kBulkSmem of dynamic shared memory). Multi-row
+// descriptors (column shards: rows of 2-14 KiB) stay on the LDG/STG row kernel,
+// where 32 lanes share the per-row address work.
+constexpr int kBulkWhich = 4;
+static bool is_bulk(int kind, int which) { return kind == K_COPY1 && which == kBulkWhich; }
+
 template <class P>
 static auto kernel_of(int kind, int which) -> void (*)(P) {
+  if (is_bulk(kind, which)) return bulk_kernel<P>;
   switch (kind) {
     case K_COPY1: return kernel_for<P, K_COPY1>(which);
     case K_BF16_F16: return kernel_for<P, K_BF16_F16>(which);
@@ -576,7 +665,7 @@ static auto kernel_of(int kind, int which) -> void (*)(P) {
     default: return kernel_for<P, K_BF16_F32>(which);
   }
 }
-constexpr int kWhich = 4;
+constexpr int kWhich = 5;  // generic, 3 row classes, bulk
 
 struct DevInfo {
   int sms = 0;
@@ -597,7 +686,15 @@ static uint64_t grid_cap(int kind, int which) {
   if (di.sms == 0) cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
   if (di.blocks_per_sm[kind][which] == 0) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(kind, which), kThreads, 0);
+    if (is_bulk(kind, which)) {
+      // one CTA per SM keeps kBulkStages chunks in flight per SM (more CTAs measured slower)
+      cudaFuncSetAttribute(kernel_of<Params>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+      cudaFuncSetAttribute(kernel_of<SmallParams>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kBulkSmem);
+      b = 1;
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(kind, which), kThreads, 0);
+    }
     di.blocks_per_sm[kind][which] = b > 0 ? b : 1;
   }
   return (uint64_t)di.sms * di.blocks_per_sm[kind][which];
@@ -644,12 +741,13 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
       k.nvec = rows * vpr;
       if (rows == 1 || vpr >= kMinRowVecs) {
         k.mode = M_ROWS;
-        const uint64_t uv = row_unit_vecs(kind);
-        k.upr = (uint32_t)((vpr + uv - 1) / uv);
-        units[*count] = rows * k.upr;
         const uint64_t g = (kind == K_F16_F32 || kind == K_BF16_F32) ? 8 : 16;  // load granule
         const bool uniform = rows == 1 || pitch % g == 0;
         k.which = 1 + (uniform ? (h.src % g == 0 ? R_ALIGNED : R_SHIFTED) : R_MIXED);
+        if (kind == K_COPY1 && rows == 1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
+        const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs : row_unit_vecs(kind);
+        k.upr = (uint32_t)((vpr + uv - 1) / uv);
+        units[*count] = rows * k.upr;
       } else {
         k.mode = M_PACKED;
         units[*count] = (k.nvec + kUnitVecs - 1) / kUnitVecs;
@@ -673,18 +771,21 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
 
 static int launch(int kind, int which, Params& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
-  const uint64_t want = (p.total_units + kWarps - 1) / kWarps;
+  const bool bulk = is_bulk(kind, which);
+  const uint64_t want = bulk ? p.total_units : (p.total_units + kWarps - 1) / kWarps;
   const uint64_t cap = grid_cap(kind, which);
   const unsigned grid = (unsigned)(want < cap ? want : cap);
+  const unsigned threads = bulk ? 32 : kThreads;
+  const size_t smem = bulk ? kBulkSmem : 0;
   if (p.n <= (uint32_t)kSmallDescs) {
     SmallParams sp;
     sp.n = p.n;
     sp.pad = 0;
     sp.total_units = p.total_units;
     for (uint32_t i = 0; i < p.n; ++i) sp.d[i] = p.d[i];
-    kernel_of<SmallParams>(kind, which)<<<grid, kThreads, 0, stream>>>(sp);
+    kernel_of<SmallParams>(kind, which)<<<grid, threads, smem, stream>>>(sp);
   } else {
-    kernel_of<Params>(kind, which)<<<grid, kThreads, 0, stream>>>(p);
+    kernel_of<Params>(kind, which)<<<grid, threads, smem, stream>>>(p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HL_ECUDA, "gather launch failed: %s", cudaGetErrorString(e));
