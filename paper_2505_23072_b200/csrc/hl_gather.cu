@@ -622,6 +622,130 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- TMA-staged realign / cast
+// Contiguous tensors whose bytes must change on the way (a cast, or a source
+// that is not 16-byte aligned): a producer thread streams each unit's aligned
+// source window HBM -> shared memory with cp.async.bulk (mbarrier "full"),
+// kConsumerWarps warps read the window out of shared memory at the tensor's
+// byte shift, convert, and store 16-byte vectors to HBM, then release the stage
+// (mbarrier "empty"). The loads no longer depend on how many vectors the
+// registers of the SM can keep in flight — the limit of the LDG/STG row kernel.
+constexpr uint32_t kStageIn = 16u << 10;             // source bytes per unit
+constexpr uint32_t kStageBytes = kStageIn + 32;      // + shift and tail granule
+constexpr int kStagedStages = 6;
+constexpr int kConsumerWarps = 8;
+constexpr int kStagedThreads = 32 * (1 + kConsumerWarps);
+constexpr size_t kStagedSmem = (size_t)kStagedStages * kStageBytes;
+__host__ __device__ constexpr uint32_t span_bytes(int kind) { return kind == 2 ? 32 : (kind >= 3 ? 8 : 16); }
+__host__ __device__ constexpr uint64_t staged_unit_vecs(int kind) { return kStageIn / span_bytes(kind); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred ready;\n"
+      "WAIT: mbarrier.try_wait.parity.shared::cta.b64 ready, [%0], %1;\n"
+      " @!ready bra WAIT;\n}\n" :: "r"(bar), "r"(parity) : "memory");
+}
+
+struct StagedUnit {
+  const uint8_t* win;  // 16-byte aligned source window
+  uint8_t* dst;
+  uint32_t wbytes;     // window bytes (multiple of 16)
+  uint32_t sh;         // byte shift of the first span inside the window
+  uint32_t nv;         // output vectors
+};
+
+template <int K, class P>
+__device__ __forceinline__ StagedUnit staged_unit(const P& p, uint64_t u, uint32_t& di) {
+  constexpr uint32_t NB = KindTraits<K>::NB;
+  constexpr uint64_t UV = staged_unit_vecs(K);
+  while (di + 1 < p.n && p.d[di + 1].unit_begin <= u) ++di;
+  const KDesc& d = p.d[di];
+  const uint64_t v0 = (u - d.unit_begin) * UV;
+  StagedUnit x;
+  x.nv = (uint32_t)min(UV, d.row_len - v0);
+  const uint64_t s0 = d.src + v0 * NB;
+  const uint64_t a0 = s0 & ~(uint64_t)15;
+  x.win = reinterpret_cast<const uint8_t*>(a0);
+  x.sh = (uint32_t)(s0 - a0);
+  x.wbytes = (uint32_t)(((s0 + (uint64_t)x.nv * NB + 15) & ~(uint64_t)15) - a0);
+  x.dst = reinterpret_cast<uint8_t*>(d.dst) + v0 * 16;
+  return x;
+}
+
+__device__ __forceinline__ uint4 lds16(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+template <int K, class P>
+__global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_constant__ P p) {
+  constexpr uint32_t NB = KindTraits<K>::NB;
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t full[kStagedStages], empty[kStagedStages];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagedStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(kConsumerWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
+  uint32_t di = 0;
+  if (warp == 0) {  // producer
+    if (lane != 0) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    for (uint64_t k = 0; k < mine; ++k) {
+      const int s = (int)(k % kStagedStages);
+      if (k >= (uint64_t)kStagedStages) mbar_wait(smem_u32(&empty[s]), (uint32_t)((k / kStagedStages - 1) & 1));
+      const StagedUnit x = staged_unit<K>(p, first + k * step, di);
+      const uint32_t b = smem_u32(&full[s]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(x.wbytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+          :: "r"(smem_u32(stage + (size_t)s * kStageBytes)), "l"(x.win), "r"(x.wbytes), "r"(b), "l"(policy)
+          : "memory");
+    }
+    return;
+  }
+  const uint32_t ct = threadIdx.x - 32;  // consumer thread
+  for (uint64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % kStagedStages);
+    const StagedUnit x = staged_unit<K>(p, first + k * step, di);
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kStagedStages) & 1));
+    const uint8_t* w = stage + (size_t)s * kStageBytes;
+    for (uint32_t v = ct; v < x.nv; v += 32 * kConsumerWarps) {
+      Span<NB> sp;
+      const uint32_t o = x.sh + v * NB;
+      if constexpr (NB == 8) {
+        const uint64_t* q = reinterpret_cast<const uint64_t*>(w + (o & ~7u));
+        const uint32_t r = o & 7;
+        uint64_t lo = q[0];
+        if (r) lo = (lo >> (8 * r)) | (q[1] << (64 - 8 * r));
+        sp.v[0] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), 0, 0);
+      } else {
+        const uint8_t* g = w + (o & ~15u);
+        const uint32_t r = o & 15;
+        if (r == 0) {
+#pragma unroll
+          for (int i = 0; i < (int)(NB / 16); ++i) sp.v[i] = lds16(g + 16 * i);
+        } else {
+          uint4 c0 = lds16(g);
+#pragma unroll
+          for (int i = 0; i < (int)(NB / 16); ++i) {
+            const uint4 c1 = lds16(g + 16 * (i + 1));
+            sp.v[i] = extract16(c0, c1, r);
+            c0 = c1;
+          }
+        }
+      }
+      stg16(x.dst + (size_t)v * 16, convert_vec<K>(sp));
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- host side
 static const uint32_t kSize[13] = {1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8};
 
@@ -653,10 +777,24 @@ static auto kernel_for(int which) -> void (*)(P) {
 // where 32 lanes share the per-row address work.
 constexpr int kBulkWhich = 4;
 static bool is_bulk(int kind, int which) { return kind == K_COPY1 && which == kBulkWhich; }
+// Contiguous casts and realigns run on the TMA-staged kernel.
+constexpr int kStagedWhich = 5;
+static bool is_staged(int which) { return which == kStagedWhich; }
+template <class P>
+static auto staged_of(int kind) -> void (*)(P) {
+  switch (kind) {
+    case K_COPY1: return staged_kernel<K_COPY1, P>;
+    case K_BF16_F16: return staged_kernel<K_BF16_F16, P>;
+    case K_F32_F16: return staged_kernel<K_F32_F16, P>;
+    case K_F16_F32: return staged_kernel<K_F16_F32, P>;
+    default: return staged_kernel<K_BF16_F32, P>;
+  }
+}
 
 template <class P>
 static auto kernel_of(int kind, int which) -> void (*)(P) {
   if (is_bulk(kind, which)) return bulk_kernel<P>;
+  if (is_staged(which)) return staged_of<P>(kind);
   switch (kind) {
     case K_COPY1: return kernel_for<P, K_COPY1>(which);
     case K_BF16_F16: return kernel_for<P, K_BF16_F16>(which);
@@ -665,7 +803,7 @@ static auto kernel_of(int kind, int which) -> void (*)(P) {
     default: return kernel_for<P, K_BF16_F32>(which);
   }
 }
-constexpr int kWhich = 5;  // generic, 3 row classes, bulk
+constexpr int kWhich = 6;  // generic, 3 row classes, bulk, staged
 
 struct DevInfo {
   int sms = 0;
@@ -686,11 +824,11 @@ static uint64_t grid_cap(int kind, int which) {
   if (di.sms == 0) cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
   if (di.blocks_per_sm[kind][which] == 0) {
     int b = 0;
-    if (is_bulk(kind, which)) {
-      // one CTA per SM keeps kBulkStages chunks in flight per SM (more CTAs measured slower)
-      cudaFuncSetAttribute(kernel_of<Params>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
-      cudaFuncSetAttribute(kernel_of<SmallParams>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kBulkSmem);
+    if (is_bulk(kind, which) || is_staged(which)) {
+      // one CTA per SM keeps its stages of chunks in flight per SM (more CTAs measured slower)
+      const int smem = (int)(is_bulk(kind, which) ? kBulkSmem : kStagedSmem);
+      cudaFuncSetAttribute(kernel_of<Params>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kernel_of<SmallParams>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       b = 1;
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(kind, which), kThreads, 0);
@@ -744,8 +882,9 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
         const uint64_t g = (kind == K_F16_F32 || kind == K_BF16_F32) ? 8 : 16;  // load granule
         const bool uniform = rows == 1 || pitch % g == 0;
         k.which = 1 + (uniform ? (h.src % g == 0 ? R_ALIGNED : R_SHIFTED) : R_MIXED);
-        if (kind == K_COPY1 && rows == 1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
-        const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs : row_unit_vecs(kind);
+        if (rows == 1) k.which = (kind == K_COPY1 && k.which == 1 + R_ALIGNED) ? kBulkWhich : kStagedWhich;
+        const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs
+                            : is_staged(k.which) ? staged_unit_vecs(kind) : row_unit_vecs(kind);
         k.upr = (uint32_t)((vpr + uv - 1) / uv);
         units[*count] = rows * k.upr;
       } else {
@@ -771,12 +910,12 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
 
 static int launch(int kind, int which, Params& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
-  const bool bulk = is_bulk(kind, which);
-  const uint64_t want = bulk ? p.total_units : (p.total_units + kWarps - 1) / kWarps;
+  const bool bulk = is_bulk(kind, which), staged = is_staged(which);
+  const uint64_t want = (bulk || staged) ? p.total_units : (p.total_units + kWarps - 1) / kWarps;
   const uint64_t cap = grid_cap(kind, which);
   const unsigned grid = (unsigned)(want < cap ? want : cap);
-  const unsigned threads = bulk ? 32 : kThreads;
-  const size_t smem = bulk ? kBulkSmem : 0;
+  const unsigned threads = bulk ? 32 : staged ? kStagedThreads : kThreads;
+  const size_t smem = bulk ? kBulkSmem : staged ? kStagedSmem : 0;
   if (p.n <= (uint32_t)kSmallDescs) {
     SmallParams sp;
     sp.n = p.n;
