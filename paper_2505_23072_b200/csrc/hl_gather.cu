@@ -633,7 +633,8 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
 constexpr uint32_t kStageIn = 16u << 10;             // source bytes per unit
 constexpr uint32_t kStageBytes = kStageIn + 32;      // + shift and tail granule
 constexpr int kStagedStages = 6;
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;
+constexpr int kStagedCtasPerSm = 2;  // 2 x (1 + 16) warps and 2 x 96 KiB of stages per SM
 constexpr int kStagedThreads = 32 * (1 + kConsumerWarps);
 constexpr size_t kStagedSmem = (size_t)kStagedStages * kStageBytes;
 __host__ __device__ constexpr uint32_t span_bytes(int kind) { return kind == 2 ? 32 : (kind >= 3 ? 8 : 16); }
@@ -714,32 +715,44 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
     const StagedUnit x = staged_unit<K>(p, first + k * step, di);
     mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kStagedStages) & 1));
     const uint8_t* w = stage + (size_t)s * kStageBytes;
-    for (uint32_t v = ct; v < x.nv; v += 32 * kConsumerWarps) {
-      Span<NB> sp;
+    // every consumer thread owns CU vectors of the unit: all their shared-memory
+    // reads are issued before the first conversion (ILP across the vectors)
+    constexpr uint32_t CT = 32 * kConsumerWarps;
+    constexpr uint32_t CU = (uint32_t)((staged_unit_vecs(K) + CT - 1) / CT);
+    Span<NB> sp[CU];
+#pragma unroll
+    for (uint32_t i = 0; i < CU; ++i) {
+      const uint32_t v = ct + i * CT;
+      if (v >= x.nv) break;
       const uint32_t o = x.sh + v * NB;
       if constexpr (NB == 8) {
         const uint64_t* q = reinterpret_cast<const uint64_t*>(w + (o & ~7u));
         const uint32_t r = o & 7;
         uint64_t lo = q[0];
         if (r) lo = (lo >> (8 * r)) | (q[1] << (64 - 8 * r));
-        sp.v[0] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), 0, 0);
+        sp[i].v[0] = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), 0, 0);
       } else {
         const uint8_t* g = w + (o & ~15u);
         const uint32_t r = o & 15;
         if (r == 0) {
 #pragma unroll
-          for (int i = 0; i < (int)(NB / 16); ++i) sp.v[i] = lds16(g + 16 * i);
+          for (int j = 0; j < (int)(NB / 16); ++j) sp[i].v[j] = lds16(g + 16 * j);
         } else {
           uint4 c0 = lds16(g);
 #pragma unroll
-          for (int i = 0; i < (int)(NB / 16); ++i) {
-            const uint4 c1 = lds16(g + 16 * (i + 1));
-            sp.v[i] = extract16(c0, c1, r);
+          for (int j = 0; j < (int)(NB / 16); ++j) {
+            const uint4 c1 = lds16(g + 16 * (j + 1));
+            sp[i].v[j] = extract16(c0, c1, r);
             c0 = c1;
           }
         }
       }
-      stg16(x.dst + (size_t)v * 16, convert_vec<K>(sp));
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < CU; ++i) {
+      const uint32_t v = ct + i * CT;
+      if (v >= x.nv) break;
+      stg16(x.dst + (size_t)v * 16, convert_vec<K>(sp[i]));
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
@@ -825,11 +838,12 @@ static uint64_t grid_cap(int kind, int which) {
   if (di.blocks_per_sm[kind][which] == 0) {
     int b = 0;
     if (is_bulk(kind, which) || is_staged(which)) {
-      // one CTA per SM keeps its stages of chunks in flight per SM (more CTAs measured slower)
+      // bulk: one CTA per SM keeps its stages in flight (more CTAs measured slower);
+      // staged: two, so 32 consumer warps per SM hide the conversion latency
       const int smem = (int)(is_bulk(kind, which) ? kBulkSmem : kStagedSmem);
       cudaFuncSetAttribute(kernel_of<Params>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(kernel_of<SmallParams>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      b = 1;
+      b = is_bulk(kind, which) ? 1 : kStagedCtasPerSm;
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel_of<Params>(kind, which), kThreads, 0);
     }
@@ -882,7 +896,10 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
         const uint64_t g = (kind == K_F16_F32 || kind == K_BF16_F32) ? 8 : 16;  // load granule
         const bool uniform = rows == 1 || pitch % g == 0;
         k.which = 1 + (uniform ? (h.src % g == 0 ? R_ALIGNED : R_SHIFTED) : R_MIXED);
-        if (rows == 1) k.which = (kind == K_COPY1 && k.which == 1 + R_ALIGNED) ? kBulkWhich : kStagedWhich;
+        // contiguous: aligned raw copies -> TMA bulk; misaligned sources -> TMA-staged
+        // (aligned casts measured faster on the LDG/STG row kernel: 6.05 vs 5.72 TB/s bf16->f16)
+        if (rows == 1 && kind == K_COPY1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
+        if (rows == 1 && k.which == 1 + R_SHIFTED) k.which = kStagedWhich;
         const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs
                             : is_staged(k.which) ? staged_unit_vecs(kind) : row_unit_vecs(kind);
         k.upr = (uint32_t)((vpr + uv - 1) / uv);
