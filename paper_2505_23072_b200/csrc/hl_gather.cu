@@ -630,11 +630,27 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
 // byte shift, convert, and store 16-byte vectors to HBM, then release the stage
 // (mbarrier "empty"). The loads no longer depend on how many vectors the
 // registers of the SM can keep in flight — the limit of the LDG/STG row kernel.
-constexpr uint32_t kStageIn = 16u << 10;             // source bytes per unit
+// (the HL_STAGED_* macros exist for tuning sweeps: tools/staged_sweep.sh)
+#ifndef HL_STAGED_IN_KB
+#define HL_STAGED_IN_KB 16
+#endif
+#ifndef HL_STAGED_STAGES
+#define HL_STAGED_STAGES 6
+#endif
+#ifndef HL_STAGED_WARPS
+#define HL_STAGED_WARPS 16
+#endif
+#ifndef HL_STAGED_CTAS
+#define HL_STAGED_CTAS 2
+#endif
+#ifndef HL_STAGED_ALIGNED
+#define HL_STAGED_ALIGNED 0
+#endif
+constexpr uint32_t kStageIn = HL_STAGED_IN_KB << 10;  // source bytes per unit
 constexpr uint32_t kStageBytes = kStageIn + 32;      // + shift and tail granule
-constexpr int kStagedStages = 6;
-constexpr int kConsumerWarps = 16;
-constexpr int kStagedCtasPerSm = 2;  // 2 x (1 + 16) warps and 2 x 96 KiB of stages per SM
+constexpr int kStagedStages = HL_STAGED_STAGES;
+constexpr int kConsumerWarps = HL_STAGED_WARPS;
+constexpr int kStagedCtasPerSm = HL_STAGED_CTAS;  // 2 x (1 + 16) warps and 2 x 96 KiB of stages per SM
 constexpr int kStagedThreads = 32 * (1 + kConsumerWarps);
 constexpr size_t kStagedSmem = (size_t)kStagedStages * kStageBytes;
 __host__ __device__ constexpr uint32_t span_bytes(int kind) { return kind == 2 ? 32 : (kind >= 3 ? 8 : 16); }
@@ -899,7 +915,8 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
         // contiguous: aligned raw copies -> TMA bulk; misaligned sources -> TMA-staged
         // (aligned casts measured faster on the LDG/STG row kernel: 6.05 vs 5.72 TB/s bf16->f16)
         if (rows == 1 && kind == K_COPY1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
-        if (rows == 1 && k.which == 1 + R_SHIFTED) k.which = kStagedWhich;
+        if (rows == 1 && (k.which == 1 + R_SHIFTED || (HL_STAGED_ALIGNED && k.which == 1 + R_ALIGNED)))
+          k.which = kStagedWhich;
         const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs
                             : is_staged(k.which) ? staged_unit_vecs(kind) : row_unit_vecs(kind);
         k.upr = (uint32_t)((vpr + uv - 1) / uv);
