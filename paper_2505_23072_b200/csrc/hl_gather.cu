@@ -31,6 +31,12 @@
 //   * Element path: rows whose output length is not a multiple of 16 bytes
 //     (odd shard widths, tiny tensors, tails) fall back to per-element moves.
 //     Correct for every case the reference accepts; never hot for LLM shapes.
+//   * Contiguous descriptors skip the warp units: aligned raw copies go to
+//     bulk_kernel (TMA cp.async.bulk HBM -> smem -> HBM, one issuing thread per
+//     SM), misaligned sources to staged_kernel (TMA loads into smem stages,
+//     consumer warps shift/convert/store). Both stride 16 KiB units per CTA.
+//     Aligned casts and multi-row (column shard) descriptors stay on the warp
+//     kernels above.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
