@@ -658,9 +658,20 @@ constexpr int kStagedStages = HL_STAGED_STAGES;
 constexpr int kConsumerWarps = HL_STAGED_WARPS;
 constexpr int kStagedCtasPerSm = HL_STAGED_CTAS;  // 2 x (1 + 16) warps and 2 x 96 KiB of stages per SM
 constexpr int kStagedThreads = 32 * (1 + kConsumerWarps);
-constexpr size_t kStagedSmem = (size_t)kStagedStages * kStageBytes;
+#ifndef HL_STAGED_TMA_STORE
+#define HL_STAGED_TMA_STORE 0
+#endif
 __host__ __device__ constexpr uint32_t span_bytes(int kind) { return kind == 2 ? 32 : (kind >= 3 ? 8 : 16); }
 __host__ __device__ constexpr uint64_t staged_unit_vecs(int kind) { return kStageIn / span_bytes(kind); }
+// optional output staging: consumers write the unit to shared memory and the
+// producer bulk-stores it (narrowing / same-size kinds only: widening doubles it)
+__host__ __device__ constexpr bool staged_tma_store(int kind) { return HL_STAGED_TMA_STORE && span_bytes(kind) >= 16; }
+__host__ __device__ constexpr uint32_t staged_out_bytes(int kind) {
+  return staged_tma_store(kind) ? (uint32_t)(staged_unit_vecs(kind) * 16) : 0;
+}
+__host__ __device__ constexpr size_t staged_smem(int kind) {
+  return (size_t)kStagedStages * (kStageBytes + staged_out_bytes(kind));
+}
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -700,7 +711,10 @@ __device__ __forceinline__ uint4 lds16(const uint8_t* p) { return *reinterpret_c
 template <int K, class P>
 __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_constant__ P p) {
   constexpr uint32_t NB = KindTraits<K>::NB;
+  constexpr bool TS = staged_tma_store(K);
+  constexpr uint32_t OUTB = staged_out_bytes(K);
   extern __shared__ __align__(128) uint8_t stage[];
+  uint8_t* const outs = stage + (size_t)kStagedStages * kStageBytes;  // TS: output stage s at outs + s * OUTB
   __shared__ __align__(8) uint64_t full[kStagedStages], empty[kStagedStages];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -718,9 +732,8 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
     if (lane != 0) return;
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-    for (uint64_t k = 0; k < mine; ++k) {
+    auto load = [&](uint64_t k) {
       const int s = (int)(k % kStagedStages);
-      if (k >= (uint64_t)kStagedStages) mbar_wait(smem_u32(&empty[s]), (uint32_t)((k / kStagedStages - 1) & 1));
       const StagedUnit x = staged_unit<K>(p, first + k * step, di);
       const uint32_t b = smem_u32(&full[s]);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(x.wbytes) : "memory");
@@ -728,6 +741,30 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
           :: "r"(smem_u32(stage + (size_t)s * kStageBytes)), "l"(x.win), "r"(x.wbytes), "r"(b), "l"(policy)
           : "memory");
+    };
+    if constexpr (!TS) {
+      for (uint64_t k = 0; k < mine; ++k) {
+        if (k >= (uint64_t)kStagedStages)
+          mbar_wait(smem_u32(&empty[k % kStagedStages]), (uint32_t)((k / kStagedStages - 1) & 1));
+        load(k);
+      }
+    } else {
+      uint32_t sdi = 0;
+      for (uint64_t k = 0; k < mine && k < (uint64_t)kStagedStages; ++k) load(k);
+      for (uint64_t k = 0; k < mine; ++k) {
+        const int s = (int)(k % kStagedStages);
+        mbar_wait(smem_u32(&empty[s]), (uint32_t)((k / kStagedStages) & 1));  // unit k converted
+        const StagedUnit x = staged_unit<K>(p, first + k * step, sdi);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                     :: "l"(x.dst), "r"(smem_u32(outs + (size_t)s * OUTB)), "r"(x.nv * 16u), "l"(policy)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (k + kStagedStages < mine) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // output stage s read out
+          load(k + kStagedStages);
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     return;
   }
@@ -774,8 +811,14 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
     for (uint32_t i = 0; i < CU; ++i) {
       const uint32_t v = ct + i * CT;
       if (v >= x.nv) break;
-      stg16(x.dst + (size_t)v * 16, convert_vec<K>(sp[i]));
+      if constexpr (TS) {
+        *reinterpret_cast<uint4*>(outs + (size_t)s * OUTB + (size_t)v * 16) = convert_vec<K>(sp[i]);
+      } else {
+        stg16(x.dst + (size_t)v * 16, convert_vec<K>(sp[i]));
+      }
     }
+    // generic-proxy smem writes must be visible to the async proxy (the bulk store)
+    if constexpr (TS) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
   }
@@ -862,7 +905,7 @@ static uint64_t grid_cap(int kind, int which) {
     if (is_bulk(kind, which) || is_staged(which)) {
       // bulk: one CTA per SM keeps its stages in flight (more CTAs measured slower);
       // staged: two, so 32 consumer warps per SM hide the conversion latency
-      const int smem = (int)(is_bulk(kind, which) ? kBulkSmem : kStagedSmem);
+      const int smem = (int)(is_bulk(kind, which) ? kBulkSmem : staged_smem(kind));
       cudaFuncSetAttribute(kernel_of<Params>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaFuncSetAttribute(kernel_of<SmallParams>(kind, which), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       b = is_bulk(kind, which) ? 1 : kStagedCtasPerSm;
@@ -955,7 +998,7 @@ static int launch(int kind, int which, Params& p, cudaStream_t stream) {
   const uint64_t cap = grid_cap(kind, which);
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   const unsigned threads = bulk ? 32 : staged ? kStagedThreads : kThreads;
-  const size_t smem = bulk ? kBulkSmem : staged ? kStagedSmem : 0;
+  const size_t smem = bulk ? kBulkSmem : staged ? staged_smem(kind) : 0;
   if (p.n <= (uint32_t)kSmallDescs) {
     SmallParams sp;
     sp.n = p.n;
