@@ -633,9 +633,14 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
 // that is not 16-byte aligned): a producer thread streams each unit's aligned
 // source window HBM -> shared memory with cp.async.bulk (mbarrier "full"),
 // kConsumerWarps warps read the window out of shared memory at the tensor's
-// byte shift, convert, and store 16-byte vectors to HBM, then release the stage
-// (mbarrier "empty"). The loads no longer depend on how many vectors the
-// registers of the SM can keep in flight — the limit of the LDG/STG row kernel.
+// byte shift, convert, and write the unit's output into a shared-memory output
+// stage, then release the stage (mbarrier "empty"); the producer bulk-stores the
+// output stage to HBM (cp.async.bulk bulk_group) and refills the input stage once
+// that store has read it. Widening casts (output twice the input) store 16-byte
+// vectors from the consumers instead. Neither loads nor stores depend on how many
+// vectors the registers of the SM keep in flight — the limit of the LDG/STG row
+// kernel. Used for every contiguous source that is misaligned, and for aligned
+// narrowing casts (bf16/f32 -> f16: 6.41 / 6.76 TB/s vs 6.07 / 6.16 on the row kernel).
 // (the HL_STAGED_* macros exist for tuning sweeps: tools/staged_sweep.sh)
 #ifndef HL_STAGED_IN_KB
 #define HL_STAGED_IN_KB 16
@@ -649,17 +654,20 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
 #ifndef HL_STAGED_CTAS
 #define HL_STAGED_CTAS 2
 #endif
+#ifndef HL_STAGED_STAGES_TS
+#define HL_STAGED_STAGES_TS 3
+#endif
 #ifndef HL_STAGED_ALIGNED
-#define HL_STAGED_ALIGNED 0
+#define HL_STAGED_ALIGNED 1
 #endif
 constexpr uint32_t kStageIn = HL_STAGED_IN_KB << 10;  // source bytes per unit
 constexpr uint32_t kStageBytes = kStageIn + 32;      // + shift and tail granule
-constexpr int kStagedStages = HL_STAGED_STAGES;
+constexpr int kStagedStagesMax = HL_STAGED_STAGES > HL_STAGED_STAGES_TS ? HL_STAGED_STAGES : HL_STAGED_STAGES_TS;
 constexpr int kConsumerWarps = HL_STAGED_WARPS;
-constexpr int kStagedCtasPerSm = HL_STAGED_CTAS;  // 2 x (1 + 16) warps and 2 x 96 KiB of stages per SM
+constexpr int kStagedCtasPerSm = HL_STAGED_CTAS;  // 2 x (1 + 16) warps and 2 x <= 113 KiB of stages per SM
 constexpr int kStagedThreads = 32 * (1 + kConsumerWarps);
 #ifndef HL_STAGED_TMA_STORE
-#define HL_STAGED_TMA_STORE 0
+#define HL_STAGED_TMA_STORE 1
 #endif
 __host__ __device__ constexpr uint32_t span_bytes(int kind) { return kind == 2 ? 32 : (kind >= 3 ? 8 : 16); }
 __host__ __device__ constexpr uint64_t staged_unit_vecs(int kind) { return kStageIn / span_bytes(kind); }
@@ -669,8 +677,12 @@ __host__ __device__ constexpr bool staged_tma_store(int kind) { return HL_STAGED
 __host__ __device__ constexpr uint32_t staged_out_bytes(int kind) {
   return staged_tma_store(kind) ? (uint32_t)(staged_unit_vecs(kind) * 16) : 0;
 }
+// stages in flight: input + output stages share the 2 x ~113 KiB per SM when the output is staged
+__host__ __device__ constexpr int staged_stages(int kind) {
+  return staged_tma_store(kind) ? HL_STAGED_STAGES_TS : HL_STAGED_STAGES;
+}
 __host__ __device__ constexpr size_t staged_smem(int kind) {
-  return (size_t)kStagedStages * (kStageBytes + staged_out_bytes(kind));
+  return (size_t)staged_stages(kind) * (kStageBytes + staged_out_bytes(kind));
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -713,9 +725,10 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
   constexpr uint32_t NB = KindTraits<K>::NB;
   constexpr bool TS = staged_tma_store(K);
   constexpr uint32_t OUTB = staged_out_bytes(K);
+  constexpr int kStagedStages = staged_stages(K);
   extern __shared__ __align__(128) uint8_t stage[];
   uint8_t* const outs = stage + (size_t)kStagedStages * kStageBytes;  // TS: output stage s at outs + s * OUTB
-  __shared__ __align__(8) uint64_t full[kStagedStages], empty[kStagedStages];
+  __shared__ __align__(8) uint64_t full[kStagedStagesMax], empty[kStagedStagesMax];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagedStages; ++s) {
@@ -964,7 +977,8 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
         // contiguous: aligned raw copies -> TMA bulk; misaligned sources -> TMA-staged
         // (aligned casts measured faster on the LDG/STG row kernel: 6.05 vs 5.72 TB/s bf16->f16)
         if (rows == 1 && kind == K_COPY1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
-        if (rows == 1 && (k.which == 1 + R_SHIFTED || (HL_STAGED_ALIGNED && k.which == 1 + R_ALIGNED)))
+        if (rows == 1 && (k.which == 1 + R_SHIFTED ||
+                          (HL_STAGED_ALIGNED && k.which == 1 + R_ALIGNED && staged_tma_store(kind))))
           k.which = kStagedWhich;
         const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs
                             : is_staged(k.which) ? staged_unit_vecs(kind) : row_unit_vecs(kind);
