@@ -660,8 +660,7 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
 #ifndef HL_STAGED_ALIGNED
 #define HL_STAGED_ALIGNED 1
 #endif
-constexpr uint32_t kStageIn = HL_STAGED_IN_KB << 10;  // source bytes per unit
-constexpr uint32_t kStageBytes = kStageIn + 32;      // + shift and tail granule
+constexpr uint32_t kStageIn = HL_STAGED_IN_KB << 10;  // source bytes per unit (half for widening casts)
 constexpr int kStagedStagesMax = HL_STAGED_STAGES > HL_STAGED_STAGES_TS ? HL_STAGED_STAGES : HL_STAGED_STAGES_TS;
 constexpr int kConsumerWarps = HL_STAGED_WARPS;
 constexpr int kStagedCtasPerSm = HL_STAGED_CTAS;  // 2 x (1 + 16) warps and 2 x <= 113 KiB of stages per SM
@@ -669,11 +668,20 @@ constexpr int kStagedThreads = 32 * (1 + kConsumerWarps);
 #ifndef HL_STAGED_TMA_STORE
 #define HL_STAGED_TMA_STORE 1
 #endif
+#ifndef HL_STAGED_WIDEN_TS
+#define HL_STAGED_WIDEN_TS 1
+#endif
 __host__ __device__ constexpr uint32_t span_bytes(int kind) { return kind == 2 ? 32 : (kind >= 3 ? 8 : 16); }
-__host__ __device__ constexpr uint64_t staged_unit_vecs(int kind) { return kStageIn / span_bytes(kind); }
-// optional output staging: consumers write the unit to shared memory and the
-// producer bulk-stores it (narrowing / same-size kinds only: widening doubles it)
-__host__ __device__ constexpr bool staged_tma_store(int kind) { return HL_STAGED_TMA_STORE && span_bytes(kind) >= 16; }
+// output staging: consumers write the unit to shared memory and the producer
+// bulk-stores it; widening casts (output = 2 x input) then use half-size units
+__host__ __device__ constexpr bool staged_tma_store(int kind) {
+  return HL_STAGED_TMA_STORE && (span_bytes(kind) >= 16 || HL_STAGED_WIDEN_TS);
+}
+__host__ __device__ constexpr uint32_t stage_in(int kind) {
+  return (span_bytes(kind) == 8 && staged_tma_store(kind)) ? kStageIn / 2 : kStageIn;
+}
+__host__ __device__ constexpr uint32_t stage_bytes(int kind) { return stage_in(kind) + 32; }  // + shift, tail granule
+__host__ __device__ constexpr uint64_t staged_unit_vecs(int kind) { return stage_in(kind) / span_bytes(kind); }
 __host__ __device__ constexpr uint32_t staged_out_bytes(int kind) {
   return staged_tma_store(kind) ? (uint32_t)(staged_unit_vecs(kind) * 16) : 0;
 }
@@ -682,7 +690,7 @@ __host__ __device__ constexpr int staged_stages(int kind) {
   return staged_tma_store(kind) ? HL_STAGED_STAGES_TS : HL_STAGED_STAGES;
 }
 __host__ __device__ constexpr size_t staged_smem(int kind) {
-  return (size_t)staged_stages(kind) * (kStageBytes + staged_out_bytes(kind));
+  return (size_t)staged_stages(kind) * (stage_bytes(kind) + staged_out_bytes(kind));
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -726,6 +734,7 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
   constexpr bool TS = staged_tma_store(K);
   constexpr uint32_t OUTB = staged_out_bytes(K);
   constexpr int kStagedStages = staged_stages(K);
+  constexpr uint32_t kStageBytes = stage_bytes(K);
   extern __shared__ __align__(128) uint8_t stage[];
   uint8_t* const outs = stage + (size_t)kStagedStages * kStageBytes;  // TS: output stage s at outs + s * OUTB
   __shared__ __align__(8) uint64_t full[kStagedStagesMax], empty[kStagedStagesMax];

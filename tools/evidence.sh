@@ -16,7 +16,7 @@ for n in ${SHARED_N:-2 4}; do
 done
 # launch list of the bench command itself (cold-cache, serialised: compare shares, not absolutes)
 timeout $T ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"row_kernel|generic_kernel|bulk_kernel" -c 800 --csv --log-file gpurun_out/ncu_launches_bench.csv \
+    -k regex:"row_kernel|generic_kernel|bulk_kernel|staged_kernel" -c 800 --csv --log-file gpurun_out/ncu_launches_bench.csv \
     python bench.py --steps 2 --warmup 3 --quick --cold 0 > gpurun_out/ncu_bench_stdout.log 2>&1
 [ "${FULL_PROFILE:-1}" = 1 ] && FULL="${FULL:-clone cast castodd}" bash tools/profile.sh > gpurun_out/profile.log 2>&1
 exit 0

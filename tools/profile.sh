@@ -9,7 +9,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --log-file gpurun_out/ncu_launches.csv python tools/kernel_bench.py --variants "$V" --iters 1 \
     > gpurun_out/ncu_launches_stdout.log 2>&1
 for v in ${FULL:-clone realign castodd}; do
-  ncu --set full --clock-control none --import-source on -k regex:"row_kernel|bulk_kernel" -s 1 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"row_kernel|bulk_kernel|staged_kernel" -s 1 -c 1 \
       -o gpurun_out/prof_$v -f python tools/kernel_bench.py --variants $v --iters 1 \
       > gpurun_out/ncu_full_$v.log 2>&1
 done
