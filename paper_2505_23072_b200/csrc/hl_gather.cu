@@ -33,10 +33,10 @@
 //     Correct for every case the reference accepts; never hot for LLM shapes.
 //   * Contiguous descriptors skip the warp units: aligned raw copies go to
 //     bulk_kernel (TMA cp.async.bulk HBM -> smem -> HBM, one issuing thread per
-//     SM), misaligned sources to staged_kernel (TMA loads into smem stages,
-//     consumer warps shift/convert/store). Both stride 16 KiB units per CTA.
-//     Aligned casts and multi-row (column shard) descriptors stay on the warp
-//     kernels above.
+//     SM), casts and misaligned sources to staged_kernel (TMA loads into smem
+//     stages, consumer warps shift/convert into smem output stages, TMA bulk
+//     stores). Both stride 8-16 KiB units per CTA. Multi-row (column shard)
+//     descriptors stay on the warp kernels above.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -636,11 +636,11 @@ __global__ void __launch_bounds__(32) bulk_kernel(const __grid_constant__ P p) {
 // byte shift, convert, and write the unit's output into a shared-memory output
 // stage, then release the stage (mbarrier "empty"); the producer bulk-stores the
 // output stage to HBM (cp.async.bulk bulk_group) and refills the input stage once
-// that store has read it. Widening casts (output twice the input) store 16-byte
-// vectors from the consumers instead. Neither loads nor stores depend on how many
+// that store has read it. Widening casts (output twice the input) use half-size
+// source units so the output stage stays 16 KiB. Neither loads nor stores depend on how many
 // vectors the registers of the SM keep in flight — the limit of the LDG/STG row
-// kernel. Used for every contiguous source that is misaligned, and for aligned
-// narrowing casts (bf16/f32 -> f16: 6.41 / 6.76 TB/s vs 6.07 / 6.16 on the row kernel).
+// kernel. Used for every contiguous cast and every misaligned contiguous source
+// (bf16/f32 -> f16: 6.47 / 6.79 TB/s vs 6.07 / 6.16 on the row kernel).
 // (the HL_STAGED_* macros exist for tuning sweeps: tools/staged_sweep.sh)
 #ifndef HL_STAGED_IN_KB
 #define HL_STAGED_IN_KB 16
