@@ -730,7 +730,7 @@ def main():
         roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
                     "traffic": traffic,
-                    "kernel": (f"hl_gather row_kernel<{src_dt.value}->{cast.value}, aligned>" if cast
+                    "kernel": (f"hl_gather staged_kernel<{src_dt.value}->{cast.value}> (TMA in + out)" if cast
                                else "hl_gather bulk_kernel (TMA cp.async.bulk copy)"),
                     "launches_per_step": k_n, "algorithmic_bytes_per_launch": dom_bytes,
                     "achieved_all_launches_of_step": round(achieved_all, 1) if achieved_all else None,
