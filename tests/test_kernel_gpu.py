@@ -109,8 +109,8 @@ def test_random_batches(seed):
     assert_same(got, exp)
 
 
-@pytest.mark.parametrize("sdt,ddt", [(10, 10), (10, 9), (11, 9), (9, 11), (1, 1)])
-@pytest.mark.parametrize("shift", [0, 1, 6])
+@pytest.mark.parametrize("sdt,ddt", [(10, 10), (10, 9), (11, 9), (9, 11), (10, 11), (1, 1)])
+@pytest.mark.parametrize("shift", [0, 1, 6, 13])
 def test_large_contiguous(sdt, ddt, shift):
     rng = np.random.default_rng(7)
     n = (48 << 20) // SIZES[sdt] + 3  # ~48 MiB plus a ragged tail
@@ -199,3 +199,28 @@ def test_nccl_plane_owner_pack(world, dim, cast):
         _, exp = oracle.slice_bytes(src_bytes, out_dt.value, shape, dim, world, r)
         assert parts[r].cpu().numpy().tobytes() == exp, (r, dim, world, cast)
     assert parts[own].data_ptr() == own_out.data_ptr()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_many_multi_unit_tensors(seed):
+    """Hundreds of contiguous tensors of 1-4 TMA units (8-16 KiB source units)
+    each, every kind, random source shifts and 16-byte aligned destinations:
+    the bulk and staged kernels walk descriptor boundaries inside their stage
+    rings (each CTA sees many units; stages wrap many times)."""
+    rng = np.random.default_rng(100 + seed)
+    kinds = [(10, 10), (1, 1), (10, 9), (11, 9), (9, 11), (10, 11)]
+    src_cap = 48 << 20
+    src = rng.integers(0, 256, size=src_cap, dtype=np.uint8)
+    descs, cs, cd = [], 0, 0
+    for _ in range(900):  # > 500: several launches per kernel
+        sdt, ddt = kinds[int(rng.integers(0, len(kinds)))]
+        n = int(rng.integers(1, 4 * 16384 // SIZES[sdt]))
+        shift = int(rng.integers(0, 16)) if rng.random() < 0.5 else 0
+        so = cs + shift
+        if so + n * SIZES[sdt] > src_cap:
+            break
+        descs.append((so, cd, 1, n, n * SIZES[sdt], sdt, ddt))
+        cs = (so + n * SIZES[sdt] + 15) & ~15
+        cd = (cd + n * SIZES[ddt] + 15) & ~15
+    got, exp = run_both(src, cd, descs)
+    assert_same(got, exp)
