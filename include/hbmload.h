@@ -8,7 +8,9 @@
  * everything that touches bytes:
  *
  *   bulk file -> HBM I/O         hl_ctx_create / hl_execute_plan / hl_transfer_from_file
- *   realign / shard / cast       hl_gather (one batched sm_100a kernel, descriptor table)
+ *   realign / shard / cast       hl_gather (one batched sm_100a entry point, descriptor table;
+ *                                TMA bulk-copy / TMA-staged kernels for contiguous tensors,
+ *                                LDG/STG warp kernels for column shards)
  *   page-cache control           hl_file_residency / hl_drop_cache
  *
  * Conventions
@@ -190,7 +192,8 @@ int hl_conversion_supported(uint32_t src_dtype, uint32_t dst_dtype);
 
 /* Enqueue the whole batch on `stream` (kernel launches only: no host sync, no
  * allocation; the descriptor table travels in the launch's parameter buffer,
- * up to hl_gather_max_batch() descriptors per launch). */
+ * up to hl_gather_max_batch() descriptors per launch; one launch per kernel
+ * variant present: TMA bulk copy, TMA-staged cast/realign, row, element). */
 int hl_gather(const hl_desc* descs, uint32_t n, void* stream);
 uint32_t hl_gather_max_batch(void);
 
