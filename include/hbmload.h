@@ -200,6 +200,11 @@ uint32_t hl_gather_max_batch(void);
 /* Number of kernel launches hl_gather issued by this process so far. */
 uint64_t hl_kernel_launches(void);
 
+/* Load every hl_gather kernel variant for `device` ahead of use (CUDA loads
+ * kernels lazily): call once per process, e.g. on a side thread while the first
+ * transfer runs. Idempotent; no launches. */
+int hl_gather_prepare(int device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,7 @@ SIGNATURES = {
     "hl_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
     "hl_gather_max_batch": (C.c_uint32, []),
     "hl_kernel_launches": (C.c_uint64, []),
+    "hl_gather_prepare": (C.c_int, [C.c_int]),
 }
 
 _lib = None
@@ -145,6 +146,18 @@ def conversion_supported(src_code: int, dst_code: int) -> bool:
 
 def kernel_launches() -> int:
     return int(load().hl_kernel_launches())
+
+
+_prepared: set[int] = set()
+
+
+def gather_prepare(device: int) -> None:
+    """Load the hl_gather kernels for ``device`` ahead of their first launch
+    (once per process; ctypes drops the GIL, so this overlaps a transfer)."""
+    if device in _prepared:
+        return
+    check(load().hl_gather_prepare(device))
+    _prepared.add(device)
 
 
 _DESC = struct.Struct("<5Q2I")  # hl_desc, include/hbmload.h (48 bytes, no padding)

@@ -1050,6 +1050,29 @@ extern "C" uint32_t hl_gather_max_batch(void) { return kMaxDescs; }
 
 extern "C" uint64_t hl_kernel_launches(void) { return g_launches.load(); }
 
+extern "C" int hl_gather_prepare(int device) {
+  // Load every kernel variant and set its launch attributes ahead of the first
+  // hl_gather (CUDA loads kernels lazily, on first use): the loader calls this
+  // on a side thread while the first file transfer runs, so a fresh process's
+  // first retrievals do not pay the module loading.
+  clear_error();
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_error(HL_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  for (int kind = 0; kind < 5; ++kind) {
+    for (int which = 0; which < kWhich; ++which) {
+      if (which == kBulkWhich && kind != K_COPY1) continue;  // bulk copies only
+      cudaFuncAttributes a;
+      cudaFuncGetAttributes(&a, kernel_of<SmallParams>(kind, which));
+      grid_cap(kind, which);  // the Params variant: occupancy / shared-memory attributes
+    }
+  }
+  cudaGetLastError();
+  cudaSetDevice(prev);
+  return HL_OK;
+}
+
 extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
   clear_error();
   if (n && !descs) return set_error(HL_EINVAL, "null descriptor table");
