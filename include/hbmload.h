@@ -195,6 +195,13 @@ int hl_conversion_supported(uint32_t src_dtype, uint32_t dst_dtype);
  * up to hl_gather_max_batch() descriptors per launch; one launch per kernel
  * variant present: TMA bulk copy, TMA-staged cast/realign, row, element). */
 int hl_gather(const hl_desc* descs, uint32_t n, void* stream);
+
+/* hl_gather with flags. HL_GATHER_NO_TMA keeps every descriptor on the LDG/STG
+ * warp kernels: the loader sets it when sources are another GPU's memory (peer
+ * pulls over NVLink), whose rate is set by the link, not by the copy engine of
+ * the SM. hl_gather(d, n, s) == hl_gather_ex(d, n, s, 0). */
+#define HL_GATHER_NO_TMA 1u
+int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint32_t flags);
 uint32_t hl_gather_max_batch(void);
 
 /* Number of kernel launches hl_gather issued by this process so far. */

@@ -101,6 +101,7 @@ SIGNATURES = {
     "hl_gds_available": (C.c_int, []),
     "hl_conversion_supported": (C.c_int, [C.c_uint32, C.c_uint32]),
     "hl_gather": (C.c_int, [C.POINTER(hl_desc), C.c_uint32, C.c_void_p]),
+    "hl_gather_ex": (C.c_int, [C.POINTER(hl_desc), C.c_uint32, C.c_void_p, C.c_uint32]),
     "hl_ipc_export": (C.c_int, [C.c_void_p, C.POINTER(hl_ipc_handle)]),
     "hl_ipc_import": (C.c_int, [C.POINTER(hl_ipc_handle), C.c_int, C.POINTER(C.c_void_p)]),
     "hl_ipc_release": (C.c_int, [C.c_void_p]),
@@ -173,14 +174,21 @@ def pack(descs: list[tuple]):
     return (hl_desc * len(descs)).from_buffer_copy(b"".join([_DESC.pack(*d) for d in descs])), len(descs)
 
 
-def launch(table, n: int, stream_ptr: int) -> None:
-    check((_lib or load()).hl_gather(table, n, C.c_void_p(stream_ptr)))
+GATHER_NO_TMA = 1  # include/hbmload.h HL_GATHER_NO_TMA
 
 
-def gather(descs: list[tuple], stream_ptr: int) -> None:
+def launch(table, n: int, stream_ptr: int, flags: int = 0) -> None:
+    lib = _lib or load()
+    if flags:
+        check(lib.hl_gather_ex(table, n, C.c_void_p(stream_ptr), flags))
+    else:
+        check(lib.hl_gather(table, n, C.c_void_p(stream_ptr)))
+
+
+def gather(descs: list[tuple], stream_ptr: int, flags: int = 0) -> None:
     """Enqueue ``[(src, dst, rows, row_elems, src_pitch, src_code, dst_code), ...]``."""
     if descs:
-        launch(*pack(descs), stream_ptr)
+        launch(*pack(descs), stream_ptr, flags)
 
 
 class IoEngine:

@@ -90,9 +90,8 @@ def clone_full(view, pool, name: str, dtype: DType | None = None):
     (ref collective.py:313-315 and loader.py:490-499)."""
     dtype = dtype or view.dtype
     buf, out = _fresh(pool, name, dtype, view.shape)
-    src_ptr, keep = _source_ptr(view, pool.device)
-    kernels.run([kernels.copy_desc(src_ptr, buf.ptr, view.numel, view.dtype, dtype)], pool.device)
-    del keep  # stream-ordered: the caching allocator reuses it only for later work
+    src_ptr, peer = _source_ptr(view, pool.device)
+    kernels.run([kernels.copy_desc(src_ptr, buf.ptr, view.numel, view.dtype, dtype)], pool.device, peer)
     return buf, out
 
 
@@ -101,22 +100,22 @@ def clone_slice(view, dim: int, lo: int, hi: int, part_shape, pool, name: str, d
     (ref collective.py:318-330), optionally cast in the same pass."""
     dtype = dtype or view.dtype
     buf, out = _fresh(pool, name, dtype, part_shape)
-    src_ptr, keep = _source_ptr(view, pool.device)
-    kernels.run([kernels.shard_desc(src_ptr, view.shape, dim, lo, hi, buf.ptr, view.dtype, dtype)], pool.device)
-    del keep
+    src_ptr, peer = _source_ptr(view, pool.device)
+    kernels.run([kernels.shard_desc(src_ptr, view.shape, dim, lo, hi, buf.ptr, view.dtype, dtype)], pool.device, peer)
     return buf, out
 
 
-def _source_ptr(view, device: torch.device) -> int:
-    """Device address of ``view`` readable from ``device``. Another GPU of the
-    same process is read in place over NVLink (peer access), so the kernel on
-    the receiving GPU does the transfer and the slice/cast in one pass."""
+def _source_ptr(view, device: torch.device) -> tuple[int, bool]:
+    """Device address of ``view`` readable from ``device``, and whether it is
+    another GPU's memory. Another GPU of the same process is read in place
+    over NVLink (peer access), so the kernel on the receiving GPU does the
+    transfer and the slice/cast in one pass."""
     src_dev = view.buffer.tensor.device
     if src_dev != device:
         from . import _native
 
         _native.enable_peer_access(device.index, src_dev.index)
-    return view.buffer.ptr + view.base_offset, None
+    return view.buffer.ptr + view.base_offset, src_dev != device
 
 
 def pack_parts(spec: ShardSpec, src_ptr: int, in_dtype: DType, out_dtype: DType, own: int,
@@ -369,7 +368,7 @@ class DistGroup:
             if handles[peer] is not None:
                 ptr = _native.ipc_import(handles[peer], self.device.index)
                 out = torch.zeros(4096, dtype=torch.uint8, device=self.device)
-                kernels.run([kernels.copy_desc(ptr, out.data_ptr(), 4096, DType.U8)], self.device)
+                kernels.run([kernels.copy_desc(ptr, out.data_ptr(), 4096, DType.U8)], self.device, peer=True)
                 torch.cuda.synchronize(self.device)
                 ok = bool((out == (peer + 1) % 256).all().item())
         except Exception:  # noqa: BLE001

@@ -942,7 +942,7 @@ static uint64_t grid_cap(int kind, int which) {
 // Translate one ABI descriptor into kernel descriptors: the main one, plus an
 // element-path descriptor for the < 16-byte tail of a single-row copy.
 // Returns the number produced (0 = empty descriptor).
-static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units[2], int* count) {
+static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units[2], int* count, bool tma) {
   *count = 0;
   const int kind = conversion_kind(h.src_dtype, h.dst_dtype);
   if (kind < 0) return set_error(HL_ECONV, "unsupported conversion %u -> %u (descriptor %u)", h.src_dtype, h.dst_dtype, i);
@@ -985,8 +985,8 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
         k.which = 1 + (uniform ? (h.src % g == 0 ? R_ALIGNED : R_SHIFTED) : R_MIXED);
         // contiguous: aligned raw copies -> TMA bulk; misaligned sources -> TMA-staged
         // (aligned casts measured faster on the LDG/STG row kernel: 6.05 vs 5.72 TB/s bf16->f16)
-        if (rows == 1 && kind == K_COPY1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
-        if (rows == 1 && (k.which == 1 + R_SHIFTED ||
+        if (tma && rows == 1 && kind == K_COPY1 && k.which == 1 + R_ALIGNED) k.which = kBulkWhich;
+        if (tma && rows == 1 && (k.which == 1 + R_SHIFTED ||
                           (HL_STAGED_ALIGNED && k.which == 1 + R_ALIGNED && staged_tma_store(kind))))
           k.which = kStagedWhich;
         const uint64_t uv = is_bulk(kind, k.which) ? kBulkVecs
@@ -1073,8 +1073,11 @@ extern "C" int hl_gather_prepare(int device) {
   return HL_OK;
 }
 
-extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
+extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) { return hl_gather_ex(descs, n, stream, 0); }
+
+extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint32_t flags) {
   clear_error();
+  const bool tma = !(flags & HL_GATHER_NO_TMA);
   if (n && !descs) return set_error(HL_EINVAL, "null descriptor table");
   // translate + validate everything once, before launching anything
   static thread_local std::vector<KDesc> kds;
@@ -1088,7 +1091,7 @@ extern "C" int hl_gather(const hl_desc* descs, uint32_t n, void* stream) {
   int cnt = 0;
   uint32_t present = 0;  // bitmask of non-empty buckets
   for (uint32_t i = 0; i < n; ++i) {
-    int rc = make_kdesc(descs[i], i, kd, ku, &cnt);
+    int rc = make_kdesc(descs[i], i, kd, ku, &cnt, tma);
     if (rc) return rc;
     for (int j = 0; j < cnt; ++j) {
       const uint16_t b = (uint16_t)(kd[j].kind * kWhich + kd[j].which);

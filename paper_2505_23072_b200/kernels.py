@@ -68,22 +68,24 @@ except AttributeError:  # pragma: no cover
         return torch.cuda.current_stream(index).cuda_stream
 
 
-def run(descs: list[Desc], device: torch.device) -> None:
+def run(descs: list[Desc], device: torch.device, peer: bool = False) -> None:
     """Enqueue the batch on ``device``'s current stream. hl_gather launches on
     the CURRENT device (grid sizing and the launch itself), so switch to the
-    stream's device when the caller's differs."""
+    stream's device when the caller's differs. ``peer``: some sources are
+    another GPU's memory (peer pulls) — keep them on the LDG/STG kernels."""
     if not descs:
         return
     if torch.cuda.current_device() != device.index:
         with torch.cuda.device(device):
-            return run(descs, device)
+            return run(descs, device, peer)
+    flags = _native.GATHER_NO_TMA if peer else 0
     if TIMING is None:
-        _native.gather(descs, _raw_stream(device.index))
+        _native.gather(descs, _raw_stream(device.index), flags)
         return
     stream = torch.cuda.current_stream(device)
     table, n = _native.pack(descs)  # host-side table build stays outside the timed launch
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    _native.launch(table, n, stream.cuda_stream)
+    _native.launch(table, n, stream.cuda_stream, flags)
     e1.record(stream)
     TIMING.append((e0, e1, algorithmic_bytes(descs)))

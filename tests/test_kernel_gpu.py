@@ -224,3 +224,28 @@ def test_many_multi_unit_tensors(seed):
         cd = (cd + n * SIZES[ddt] + 15) & ~15
     got, exp = run_both(src, cd, descs)
     assert_same(got, exp)
+
+
+def test_no_tma_flag_gives_identical_bytes():
+    """hl_gather_ex(..., HL_GATHER_NO_TMA) (the peer-pull path) routes contiguous
+    copies/casts to the LDG/STG kernels: same bytes as the TMA kernels."""
+    rng = np.random.default_rng(5)
+    src = rng.integers(0, 256, size=8 << 20, dtype=np.uint8)
+    descs, cs, cd = [], 0, 0
+    for sdt, ddt in [(10, 10), (1, 1), (10, 9), (11, 9), (9, 11), (10, 11)] * 4:
+        n = int(rng.integers(1, 100_000))
+        so = cs + int(rng.integers(0, 16))
+        descs.append((so, cd, 1, n, n * SIZES[sdt], sdt, ddt))
+        cs = (so + n * SIZES[sdt] + 15) & ~15
+        cd = (cd + n * SIZES[ddt] + 15) & ~15
+    dev = torch.device("cuda", 0)
+    s = torch.from_numpy(src).to(dev)
+    outs = []
+    for flags in (0, _native.GATHER_NO_TMA):
+        d = torch.full((cd + 64,), SENTINEL, dtype=torch.uint8, device=dev)
+        kd = [(s.data_ptr() + so, d.data_ptr() + do, r, re, p, sd, dd) for so, do, r, re, p, sd, dd in descs]
+        _native.gather(kd, torch.cuda.current_stream(dev).cuda_stream, flags)
+        outs.append(d.cpu().numpy())
+    assert_same(outs[1], outs[0])
+    _, exp = run_both(src, cd, descs)
+    assert_same(outs[0], exp)
