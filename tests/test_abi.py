@@ -76,6 +76,9 @@ def test_sm100a_cubin_and_kernel_symbols():
     assert "row_kernel" in sass and "generic_kernel" in sass
     assert "LDG.E.128" in sass or "LDG.E.ENL2.128" in sass or re.search(r"LDG\.E\S*\.128", sass)
     assert re.search(r"STG\.E\S*\.128", sass)
+    # the TMA kernels: bulk copies both ways and mbarrier transaction counting
+    assert "bulk_kernel" in sass and "staged_kernel" in sass
+    assert "UBLKCP.S.G" in sass and "UBLKCP.G.S" in sass and "SYNCS.ARRIVE.TRANS64" in sass
 
 
 def test_product_never_imports_the_oracle():
