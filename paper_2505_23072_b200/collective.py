@@ -13,10 +13,11 @@ Two interchangeable group types serve the loader:
   ``check_order=True`` every collective first all-gathers its (op, key, src,
   dim) descriptor and a disagreement raises ``RendezvousTimeout`` like the
   reference (collective.py:149-159).
-* :class:`ProcessGroup` — the reference's in-process group (ranks are threads
-  sharing a Condition-variable rendezvous, generation counted, poisoned on
-  timeout), kept so reference-style multi-rank tests run unchanged on one
-  GPU. Its data moves are ``hl_gather`` kernels reading the owner's buffer.
+* :class:`ProcessGroup` — the reference's in-process group contract (ranks
+  are threads; here they meet at per-rank mailboxes behind a two-phase
+  ``threading.Barrier`` that stays broken — poisoned — after a timeout,
+  abort or ordering mismatch), kept so reference-style multi-rank tests run
+  unchanged on one GPU. Its data moves are ``hl_gather`` kernels reading the owner's buffer.
 
 Partitioning (``partition``/``ShardSpec``) is the reference's arithmetic:
 equal parts, the first ``shape[dim] % W`` ranks get one more (ref 52-74).
@@ -27,7 +28,6 @@ from __future__ import annotations
 import hashlib
 import math
 import threading
-import time
 from dataclasses import dataclass
 
 import torch
@@ -170,76 +170,92 @@ def _span_of(view) -> "_Span | None":
     return None if view is None else _Span(view.buffer, view.base_offset, view.dtype, tuple(view.shape))
 
 
+class _Mailboxes:
+    """The meeting point of W thread-ranks: one mailbox slot per rank and a
+    two-phase ``threading.Barrier``. A round is: post into your slot, pass
+    phase 1 (every slot is now written), snapshot all slots, pass phase 2
+    (every rank has its snapshot, so slots may be overwritten by the next
+    round). A barrier that breaks — a rank waited longer than the timeout, or
+    someone aborted — stays broken: the group is poisoned and the recorded
+    reason is what every later call raises."""
+
+    def __init__(self, world_size: int):
+        self._barrier = threading.Barrier(world_size)
+        self._slots: list[object] = [None] * world_size
+        self._posted = [False] * world_size
+        self._lock = threading.Lock()
+        self.reason: str | None = None
+
+    def fail(self, reason: str) -> RendezvousTimeout:
+        with self._lock:
+            if self.reason is None:
+                self.reason = reason
+        self._barrier.abort()
+        return RendezvousTimeout(self.reason)
+
+    def _pass(self, rank: int, timeout: float, phase: str) -> None:
+        try:
+            self._barrier.wait(timeout)
+        except threading.BrokenBarrierError:
+            raise self.fail(f"rank {rank} timed out after {timeout}s at the {phase} barrier: "
+                            "a peer rank failed to arrive") from None
+
+    def round(self, rank: int, payload: object, timeout: float) -> dict[int, object]:
+        with self._lock:
+            if self.reason is not None:
+                raise RendezvousTimeout(self.reason)
+            twice = self._posted[rank]
+            self._posted[rank] = True
+        if twice:  # this rank is already inside a collective on another thread
+            raise self.fail(f"rank {rank} issued a collective out of turn")
+        self._slots[rank] = payload
+        try:
+            self._pass(rank, timeout, "arrive")
+            snapshot = dict(enumerate(self._slots))
+            self._pass(rank, timeout, "leave")
+        finally:
+            with self._lock:
+                self._posted[rank] = False
+        return snapshot
+
+
 class ProcessGroup:
-    """In-process ranks (threads) with rendezvous collectives (ref collective.py:77-256)."""
+    """In-process ranks (threads) with blocking collectives — the reference's
+    group contract (ref collective.py:77-256): ``exchange`` returns every
+    rank's payload on every rank, collectives carry an (op, tag, src)
+    descriptor that must agree across ranks, and a timeout, an abort or a
+    descriptor disagreement poisons the group for good (``RendezvousTimeout``).
+    The data moves are hl_gather kernels reading the owner's buffer."""
 
     def __init__(self, world_size: int, timeout: float = DEFAULT_TIMEOUT):
         if world_size < 1:
             raise ValueError(f"world_size must be >= 1, got {world_size}")
         self.world_size = world_size
         self.timeout = timeout
-        self._cv = threading.Condition()
-        self._gen = 0
-        self._slots: dict[int, object] = {}
-        self._done: dict[int, list] = {}
-        self._poison: str | None = None
+        self._boxes = _Mailboxes(world_size)
 
     def rank_ids(self) -> range:
         return range(self.world_size)
-
-    def _poison_now(self, reason: str) -> None:
-        self._poison = reason
-        self._cv.notify_all()
 
     def exchange(self, rank: int, payload: object) -> dict[int, object]:
         if not 0 <= rank < self.world_size:
             raise ValueError(f"rank {rank} not in group of {self.world_size}")
         if self.world_size == 1:
             return {0: payload}
-        with self._cv:
-            if self._poison:
-                raise RendezvousTimeout(self._poison)
-            if rank in self._slots:
-                self._poison_now(f"rank {rank} issued a collective out of turn")
-                raise RendezvousTimeout(self._poison)
-            gen = self._gen
-            self._slots[rank] = payload
-            if len(self._slots) == self.world_size:
-                self._done[gen] = [dict(self._slots), self.world_size]
-                self._slots = {}
-                self._gen += 1
-                self._cv.notify_all()
-            else:
-                deadline = time.monotonic() + self.timeout
-                while gen not in self._done and not self._poison:
-                    left = deadline - time.monotonic()
-                    if left <= 0:
-                        self._poison_now(f"rank {rank} timed out after {self.timeout}s waiting for peers "
-                                         f"(collective #{gen}); a rank failed to arrive")
-                        break
-                    self._cv.wait(left)
-                if gen not in self._done:
-                    raise RendezvousTimeout(self._poison)
-            snap, left = self._done[gen]
-            if left == 1:
-                del self._done[gen]
-            else:
-                self._done[gen][1] = left - 1
-            return snap
+        return self._boxes.round(rank, payload, self.timeout)
 
     def _checked_exchange(self, rank: int, desc: tuple, data: object) -> dict[int, object]:
-        entries = self.exchange(rank, (desc, data))
-        descs = {r: d for r, (d, _) in entries.items()}
-        if any(d != desc for d in descs.values()):
-            with self._cv:
-                self._poison_now(f"collective mismatch across ranks (ordering bug): rank {rank} issued "
-                                 f"{desc}, peers issued {sorted(set(descs.values()), key=repr)}")
-            raise RendezvousTimeout(self._poison)
-        return {r: x for r, (_, x) in entries.items()}
+        """One round carrying (descriptor, data); every rank compares all
+        descriptors, so a mismatch is seen — and raised — on every rank."""
+        got = self.exchange(rank, (desc, data))
+        others = {d for d, _ in got.values() if d != desc}
+        if others:
+            raise self._boxes.fail(f"collective mismatch across ranks (ordering bug): rank {rank} issued "
+                                   f"{desc}, peers issued {sorted(others | {desc}, key=repr)}")
+        return {r: x for r, (_, x) in got.items()}
 
     def abort(self, reason: str) -> None:
-        with self._cv:
-            self._poison_now(reason)
+        self._boxes.fail(reason)
 
     def agree(self, rank: int, src: int, value: object, tag: str = "") -> object:
         if self.world_size == 1:
