@@ -26,7 +26,8 @@
  *     default stream).
  *
  * Reference interfaces replaced (pkg/src/aggload/...):
- *   hl_execute_plan        transfer.py:305-389  execute_plan(plan, pools)
+ *   hl_execute_plan(_after) transfer.py:305-389 execute_plan(plan, pools)
+ *   hl_topology_resolve    transfer.py:51-121, 274-293  Topology / worker NUMA affinity
  *   hl_transfer_from_file  device.py:238-288    transfer_from_file(buf, dev_off, file, file_off, length, staging)
  *   hl_gather              device.py:466-534    align_and_convert(buf, landing, bounce, conversions)
  *                          device.py:551-586    convert_dtype(buf, view_meta, target, bounce)
@@ -45,7 +46,7 @@
 extern "C" {
 #endif
 
-#define HL_ABI_VERSION 1
+#define HL_ABI_VERSION 2  /* 2: hl_execute_plan_after, hl_ctx_cpus, hl_topology_resolve, stats.numa_node */
 
 /* ---- status codes (errors.py class in brackets) ---------------------------- */
 enum hl_status {
@@ -117,7 +118,7 @@ typedef struct hl_plan_stats {
   uint64_t mmap_bytes;      /* bytes DMA'd from pinned page-cache pages        */
   double ring_setup_seconds;/* pinned ring allocation charged to this call    */
   uint32_t io_mode_used;    /* bitmask of 1<<hl_io_mode actually used         */
-  uint32_t reserved;
+  int32_t numa_node;        /* node the workers and the ring are pinned to (-1: none) */
   double read_seconds;      /* sum over workers: time inside pread / cuFileRead / pinning */
   double wait_seconds;      /* sum over workers: time waiting for a ring slot's DMA      */
   double submit_seconds;    /* sum over workers: time inside cudaMemcpyAsync/EventRecord */
@@ -130,13 +131,37 @@ int hl_ctx_config(const hl_ctx* ctx, hl_config* out);
 
 /* Run every block; blocks until all bytes are resident in HBM (all H2D
  * copies complete). On failure no partial success is reported: the caller
- * discards the destination buffers (ref transfer.py:375-378). */
+ * discards the destination buffers (ref transfer.py:375-378).
+ * The engine writes HBM from its own streams: hl_execute_plan does NOT order
+ * those writes after work the caller queued earlier. Use it only for
+ * destinations no queued kernel may still read. */
 int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
                     const hl_block* blocks, uint32_t n_blocks, hl_plan_stats* stats);
+
+/* hl_execute_plan whose writes are ordered after everything enqueued on
+ * `stream` before the call (an event recorded there is waited on by every
+ * engine stream; the cuFile path waits on the host). This is what a caller
+ * with a stream-ordered allocator needs: memory recycled from a buffer that
+ * kernels queued on `stream` still read is not overwritten before they ran.
+ * NULL = the legacy default stream. The loader always uses this entry. */
+int hl_execute_plan_after(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
+                          const hl_block* blocks, uint32_t n_blocks, void* stream,
+                          hl_plan_stats* stats);
 
 /* Single range, synchronous (ref device.py:238). */
 int hl_transfer_from_file(hl_ctx* ctx, const char* path, uint64_t file_off,
                           uint64_t len, void* dev_dst);
+
+/* The CPUs the context's worker team and pinned ring are bound to (the
+ * node's sysfs cpulist intersected with the process affinity). *n_cpus gets
+ * the full count; at most `cap` are written. */
+int hl_ctx_cpus(const hl_ctx* ctx, int32_t* cpus, uint32_t cap, uint32_t* n_cpus);
+/* The placement rule without a GPU: node = requested_node if >= 0, else
+ * $HL_NUMA_NODE, else the PCI device's sysfs numa_node; CPUs as hl_ctx_cpus.
+ * sysfs is read under $HL_SYSFS_ROOT when that is set (ref transfer.py:51-121
+ * Topology / 274-293 worker affinity). */
+int hl_topology_resolve(const char* pci_bus_id, int32_t requested_node, int32_t* node, int32_t* cpus,
+                        uint32_t cap, uint32_t* n_cpus);
 
 /* Fraction of the file's pages resident in the page cache (mincore). */
 int hl_file_residency(const char* path, double* frac);

@@ -62,7 +62,7 @@ class hl_plan_stats(C.Structure):
         ("mmap_bytes", C.c_uint64),
         ("ring_setup_seconds", C.c_double),
         ("io_mode_used", C.c_uint32),
-        ("reserved", C.c_uint32),
+        ("numa_node", C.c_int32),
         ("read_seconds", C.c_double),
         ("wait_seconds", C.c_double),
         ("submit_seconds", C.c_double),
@@ -95,6 +95,11 @@ SIGNATURES = {
     "hl_ctx_config": (C.c_int, [C.c_void_p, C.POINTER(hl_config)]),
     "hl_execute_plan": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32,
                                   C.POINTER(hl_block), C.c_uint32, C.POINTER(hl_plan_stats)]),
+    "hl_execute_plan_after": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32,
+                                        C.POINTER(hl_block), C.c_uint32, C.c_void_p, C.POINTER(hl_plan_stats)]),
+    "hl_ctx_cpus": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "hl_topology_resolve": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.c_uint32, C.POINTER(C.c_uint32)]),
     "hl_transfer_from_file": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_uint64, C.c_void_p]),
     "hl_file_residency": (C.c_int, [C.c_char_p, C.POINTER(C.c_double)]),
     "hl_drop_cache": (C.c_int, [C.c_char_p]),
@@ -206,13 +211,21 @@ class IoEngine:
         check(lib.hl_ctx_config(h, C.byref(eff)))
         self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_ if f != "reserved"}
 
-    def execute(self, paths: list[str], blocks: list[tuple[int, int, int, int, int]]) -> dict:
-        """blocks: (file_index, worker_hint, file_off, len, dev_dst). Blocking."""
+    def execute(self, paths: list[str], blocks: list[tuple[int, int, int, int, int]],
+                after_stream: int | None = None) -> dict:
+        """blocks: (file_index, worker_hint, file_off, len, dev_dst). Blocking.
+        ``after_stream`` (a cudaStream_t as int, 0 = legacy default): the
+        engine's HBM writes wait for everything already queued on it
+        (hl_execute_plan_after); None = unordered (hl_execute_plan)."""
         lib = self._lib
         cpaths = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
         arr = (hl_block * len(blocks))(*[hl_block(*b) for b in blocks])
         st = hl_plan_stats()
-        check(lib.hl_execute_plan(self._h, cpaths, len(paths), arr, len(blocks), C.byref(st)))
+        if after_stream is None:
+            check(lib.hl_execute_plan(self._h, cpaths, len(paths), arr, len(blocks), C.byref(st)))
+        else:
+            check(lib.hl_execute_plan_after(self._h, cpaths, len(paths), arr, len(blocks),
+                                            C.c_void_p(after_stream), C.byref(st)))
         modes = [name for bit, name in IO_MODE_NAMES.items() if st.io_mode_used & (1 << bit)]
         return {
             "bytes": st.bytes, "seconds": st.seconds, "workers": st.workers, "blocks": st.blocks,
@@ -221,12 +234,21 @@ class IoEngine:
             "ring_setup_seconds": st.ring_setup_seconds,
             "read_seconds": st.read_seconds, "wait_seconds": st.wait_seconds,
             "submit_seconds": st.submit_seconds,
-            "io_modes": modes,
+            "io_modes": modes, "numa_node": st.numa_node,
         }
 
-    def transfer(self, path: str, file_off: int, length: int, dev_ptr: int) -> None:
-        check(self._lib.hl_transfer_from_file(self._h, os.fsencode(path), file_off, length,
-                                              C.c_void_p(dev_ptr)))
+    def cpus(self) -> list[int]:
+        """CPUs the worker team and the pinned ring are bound to ([] = unpinned)."""
+        n = C.c_uint32()
+        check(self._lib.hl_ctx_cpus(self._h, None, 0, C.byref(n)))
+        arr = (C.c_int32 * max(n.value, 1))()
+        check(self._lib.hl_ctx_cpus(self._h, arr, n.value, C.byref(n)))
+        return list(arr[:n.value])
+
+    def transfer(self, path: str, file_off: int, length: int, dev_ptr: int, after_stream: int = 0) -> None:
+        """One range, ordered after ``after_stream`` (hl_execute_plan_after)."""
+        if length:
+            self.execute([path], [(0, 0, file_off, length, dev_ptr)], after_stream=after_stream)
 
     def close(self) -> None:
         if self._h:
@@ -238,6 +260,17 @@ class IoEngine:
             self.close()
         except Exception:
             pass
+
+
+def topology_resolve(pci_bus_id: str = "", requested_node: int = -1) -> tuple[int, list[int]]:
+    """The engine's placement rule without a GPU (hl_topology_resolve):
+    (NUMA node, CPUs the workers would be pinned to)."""
+    lib = load()
+    node, n = C.c_int32(), C.c_uint32()
+    check(lib.hl_topology_resolve(pci_bus_id.encode(), requested_node, C.byref(node), None, 0, C.byref(n)))
+    arr = (C.c_int32 * max(n.value, 1))()
+    check(lib.hl_topology_resolve(pci_bus_id.encode(), requested_node, C.byref(node), arr, n.value, C.byref(n)))
+    return node.value, list(arr[:n.value])
 
 
 def file_residency(path: str) -> float:

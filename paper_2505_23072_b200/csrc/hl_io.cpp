@@ -27,6 +27,7 @@
 #include <stdlib.h>
 #include <errno.h>
 #include <fcntl.h>
+#include <pthread.h>
 #include <sched.h>
 #include <string.h>
 #include <sys/mman.h>
@@ -37,6 +38,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -103,13 +105,20 @@ static bool cufile_load(std::string* why) {
 }
 
 // ------------------------------------------------------------------ topology
-static int gpu_numa_node(int dev) {
-  char bus[32] = {0};
-  if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return -1;
-  for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
-  char path[128];
-  snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
-  FILE* f = fopen(path, "r");
+// sysfs is read under $HL_SYSFS_ROOT when set (tests build a fake multi-node
+// tree there); the NUMA node of the engine is, in order: the caller's
+// hl_config.numa_node, $HL_NUMA_NODE, the GPU's PCI node.
+static std::string sysfs_path(const char* rel) {
+  const char* root = getenv("HL_SYSFS_ROOT");
+  return std::string(root ? root : "") + rel;
+}
+
+static int pci_numa_node(const char* bus_id) {
+  std::string bus(bus_id ? bus_id : "");
+  for (auto& ch : bus) ch = (char)tolower(ch);
+  char rel[160];
+  snprintf(rel, sizeof rel, "/sys/bus/pci/devices/%s/numa_node", bus.c_str());
+  FILE* f = fopen(sysfs_path(rel).c_str(), "r");
   if (!f) return -1;
   int node = -1;
   if (fscanf(f, "%d", &node) != 1) node = -1;
@@ -117,12 +126,13 @@ static int gpu_numa_node(int dev) {
   return node;
 }
 
+// The node's CPUs (sysfs cpulist) that this process may run on; empty = no pinning.
 static std::vector<int> node_cpus(int node) {
   std::vector<int> cpus;
   if (node < 0) return cpus;
-  char path[128];
-  snprintf(path, sizeof path, "/sys/devices/system/node/node%d/cpulist", node);
-  FILE* f = fopen(path, "r");
+  char rel[128];
+  snprintf(rel, sizeof rel, "/sys/devices/system/node/node%d/cpulist", node);
+  FILE* f = fopen(sysfs_path(rel).c_str(), "r");
   if (!f) return cpus;
   char buf[4096];
   if (fgets(buf, sizeof buf, f)) {
@@ -137,7 +147,33 @@ static std::vector<int> node_cpus(int node) {
     }
   }
   fclose(f);
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  if (sched_getaffinity(0, sizeof allowed, &allowed) == 0) {
+    std::vector<int> ok;
+    for (int c : cpus)
+      if (c >= 0 && c < CPU_SETSIZE && CPU_ISSET(c, &allowed)) ok.push_back(c);
+    cpus.swap(ok);
+  }
   return cpus;
+}
+
+static int resolve_node(const char* bus_id, int requested) {
+  if (requested >= 0) return requested;
+  if (const char* e = getenv("HL_NUMA_NODE")) {
+    char* end = nullptr;
+    long v = strtol(e, &end, 10);
+    if (end != e && v >= 0) return (int)v;
+  }
+  return pci_numa_node(bus_id);
+}
+
+static void pin_to(const std::vector<int>& cpus) {
+  if (cpus.empty()) return;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  for (int c : cpus) CPU_SET(c, &set);
+  sched_setaffinity(0, sizeof set, &set);
 }
 
 }  // namespace hl
@@ -166,9 +202,17 @@ struct hl_ctx {
   uint64_t ring_bytes = 0;
   bool ring_registered = false;  // cudaHostRegister'ed malloc (else cudaHostAlloc)
   std::mutex mu;  // one plan at a time per context
+  cudaEvent_t order_ev = nullptr;  // hl_execute_plan_after: the caller's stream position
+  // Persistent worker team (threads live as long as the context): a plan is a
+  // new generation; every team thread takes part (or sits it out) and checks in.
+  std::vector<std::thread> team;
+  std::mutex team_mu;
+  std::condition_variable team_cv, team_done;
+  uint64_t team_gen = 0;
+  struct PlanRun* team_run = nullptr;
+  uint32_t team_active = 0, team_left = 0;
+  bool team_stop = false;
 };
-
-namespace {
 
 struct Chunk {
   uint32_t file;
@@ -186,6 +230,7 @@ struct FileState {
 
 struct PlanRun {
   hl_ctx* ctx;
+  cudaEvent_t order_ev = nullptr;  // every H2D waits for it (caller's stream position)
   const std::vector<Chunk>* chunks;
   std::vector<FileState>* files;
   std::atomic<size_t> cursor{0};
@@ -207,6 +252,8 @@ struct PlanRun {
     failed.store(true);
   }
 };
+
+namespace {
 
 bool pread_full(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got, int* err) {
   uint64_t done = 0;
@@ -247,12 +294,7 @@ int ensure_ring_memory(hl_ctx* ctx, double* seconds) {
     std::vector<std::thread> touchers;
     for (uint64_t i = 0; i < nt; ++i) {
       touchers.emplace_back([&, i] {
-        if (!ctx->cpus.empty()) {
-          cpu_set_t set;
-          CPU_ZERO(&set);
-          for (int c : ctx->cpus) CPU_SET(c, &set);
-          sched_setaffinity(0, sizeof set, &set);
-        }
+        pin_to(ctx->cpus);
         const uint64_t b = i * piece, e = std::min(bytes, b + piece);
         if (b < e) memset((uint8_t*)m + b, 0, e - b);
       });
@@ -303,13 +345,6 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring);
 
 void worker_main(PlanRun* run, uint32_t w) {
   hl_ctx* ctx = run->ctx;
-  cudaSetDevice(ctx->cfg.device);
-  if (!ctx->cpus.empty()) {
-    cpu_set_t set;
-    CPU_ZERO(&set);
-    for (int c : ctx->cpus) CPU_SET(c, &set);
-    sched_setaffinity(0, sizeof set, &set);
-  }
   WorkerRing& ring = ctx->rings[w];
   if (ring.slots.empty()) {
     const double t0 = now_s();
@@ -320,6 +355,17 @@ void worker_main(PlanRun* run, uint32_t w) {
     }
     if (rc) {
       run->fail(rc, hl_last_error());
+      return;
+    }
+  }
+  if (run->order_ev) {
+    // Write-after-read guard: the destination buffers come from the caller's
+    // allocator, which may hand out memory that kernels still queued on the
+    // caller's stream are about to read. No H2D of this plan starts before
+    // that stream position.
+    cudaError_t e = cudaStreamWaitEvent(ring.stream, run->order_ev, 0);
+    if (e != cudaSuccess) {
+      run->fail(HL_ECUDA, std::string("stream ordering: ") + cudaGetErrorString(e));
       return;
     }
   }
@@ -481,6 +527,46 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
   }
 }
 
+void team_thread(hl_ctx* ctx, uint32_t w) {
+  cudaSetDevice(ctx->cfg.device);
+  pin_to(ctx->cpus);
+  char name[16];
+  snprintf(name, sizeof name, "hl-io-%d-%u", ctx->cfg.device, w);
+  pthread_setname_np(pthread_self(), name);
+  uint64_t seen = 0;
+  for (;;) {
+    PlanRun* run = nullptr;
+    bool active = false;
+    {
+      std::unique_lock<std::mutex> lk(ctx->team_mu);
+      ctx->team_cv.wait(lk, [&] { return ctx->team_stop || ctx->team_gen != seen; });
+      if (ctx->team_stop) return;
+      seen = ctx->team_gen;
+      run = ctx->team_run;
+      active = w < ctx->team_active;
+    }
+    if (active) worker_main(run, w);
+    std::lock_guard<std::mutex> g(ctx->team_mu);
+    if (--ctx->team_left == 0) ctx->team_done.notify_all();
+  }
+}
+
+// Run `run` on the first `n` team threads (spawned once per context) and wait.
+void team_run(hl_ctx* ctx, PlanRun* run, uint32_t n) {
+  while (ctx->team.size() < ctx->cfg.workers) {
+    const uint32_t w = (uint32_t)ctx->team.size();
+    ctx->team.emplace_back(team_thread, ctx, w);
+  }
+  std::unique_lock<std::mutex> lk(ctx->team_mu);
+  ctx->team_run = run;
+  ctx->team_active = n;
+  ctx->team_left = (uint32_t)ctx->team.size();
+  ++ctx->team_gen;
+  ctx->team_cv.notify_all();
+  ctx->team_done.wait(lk, [&] { return ctx->team_left == 0; });
+  ctx->team_run = nullptr;
+}
+
 double residency(int fd, uint64_t size) {
   if (size == 0) return 1.0;
   void* m = mmap(nullptr, size, PROT_READ, MAP_SHARED, fd, 0);
@@ -520,8 +606,9 @@ extern "C" int hl_ctx_create(const hl_config* cfg, hl_ctx** out) {
     delete ctx;
     return set_error(HL_EINVAL, "unknown io_mode %u", cfg->io_mode);
   }
-  int node = ctx->cfg.numa_node;
-  if (node < 0) node = gpu_numa_node(ctx->cfg.device);
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, ctx->cfg.device) != cudaSuccess) bus[0] = 0;
+  const int node = resolve_node(bus, ctx->cfg.numa_node);
   ctx->cfg.numa_node = node;
   ctx->cpus = node_cpus(node);
   if (ctx->cfg.workers == 0) {
@@ -547,7 +634,14 @@ extern "C" int hl_ctx_config(const hl_ctx* ctx, hl_config* out) {
 extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
   clear_error();
   if (!ctx) return HL_OK;
+  {
+    std::lock_guard<std::mutex> g(ctx->team_mu);
+    ctx->team_stop = true;
+    ctx->team_cv.notify_all();
+  }
+  for (auto& t : ctx->team) t.join();
   cudaSetDevice(ctx->cfg.device);
+  if (ctx->order_ev) cudaEventDestroy(ctx->order_ev);
   for (auto& r : ctx->rings) {
     if (r.stream) cudaStreamSynchronize(r.stream);
     for (auto& s : r.slots) {
@@ -567,8 +661,8 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
   return HL_OK;
 }
 
-extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n_files, const hl_block* blocks,
-                               uint32_t n_blocks, hl_plan_stats* stats) {
+static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, const hl_block* blocks,
+                   uint32_t n_blocks, bool ordered, cudaStream_t after, hl_plan_stats* stats) {
   clear_error();
   if (!ctx) return set_error(HL_EINVAL, "null context");
   if (n_blocks && (!blocks || !paths)) return set_error(HL_EINVAL, "null blocks or paths");
@@ -692,6 +786,17 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
   run.ctx = ctx;
   run.chunks = &chunks;
   run.files = &files;
+  if (ordered && !chunks.empty()) {
+    cudaError_t e = ctx->order_ev ? cudaSuccess : cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->order_ev, after);
+    // cuFile writes HBM from the host thread, outside any stream: wait here
+    if (e == cudaSuccess && (mode_mask & (1u << HL_IO_CUFILE))) e = cudaEventSynchronize(ctx->order_ev);
+    if (e != cudaSuccess) {
+      close_all();
+      return set_error(HL_ECUDA, "ordering after the caller's stream: %s", cudaGetErrorString(e));
+    }
+    run.order_ev = ctx->order_ev;
+  }
   {
     double secs = 0;
     int rc = ensure_ring_memory(ctx, &secs);
@@ -702,10 +807,7 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
     run.ring_setup += secs;
   }
   const uint32_t nw = (uint32_t)std::min<size_t>(ctx->cfg.workers, std::max<size_t>(chunks.size(), 1));
-  std::vector<std::thread> threads;
-  threads.reserve(nw);
-  for (uint32_t w = 0; w < nw; ++w) threads.emplace_back(worker_main, &run, w);
-  for (auto& t : threads) t.join();
+  team_run(ctx, &run, nw);
   close_all();
   if (stats) {
     memset(stats, 0, sizeof *stats);
@@ -722,7 +824,7 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
                           (run.direct_bytes.load() ? 1u << HL_IO_DIRECT : 0u) |
                           (run.cufile_bytes.load() ? 1u << HL_IO_CUFILE : 0u) |
                           (run.mmap_bytes.load() ? 1u << HL_IO_MMAP : 0u);
-    (void)mode_mask;
+    stats->numa_node = ctx->cfg.numa_node;
     stats->read_seconds = run.read_ns.load() * 1e-9;
     stats->wait_seconds = run.wait_ns.load() * 1e-9;
     stats->submit_seconds = run.submit_ns.load() * 1e-9;
@@ -731,10 +833,40 @@ extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n
   return HL_OK;
 }
 
+extern "C" int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n_files, const hl_block* blocks,
+                               uint32_t n_blocks, hl_plan_stats* stats) {
+  return execute(ctx, paths, n_files, blocks, n_blocks, false, nullptr, stats);
+}
+
+extern "C" int hl_execute_plan_after(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
+                                     const hl_block* blocks, uint32_t n_blocks, void* stream,
+                                     hl_plan_stats* stats) {
+  return execute(ctx, paths, n_files, blocks, n_blocks, true, (cudaStream_t)stream, stats);
+}
+
 extern "C" int hl_transfer_from_file(hl_ctx* ctx, const char* path, uint64_t file_off, uint64_t len, void* dev_dst) {
   hl_block b{0, 0, file_off, len, (uint64_t)(uintptr_t)dev_dst};
   if (len == 0) return HL_OK;
   return hl_execute_plan(ctx, &path, 1, &b, 1, nullptr);
+}
+
+extern "C" int hl_ctx_cpus(const hl_ctx* ctx, int32_t* cpus, uint32_t cap, uint32_t* n_cpus) {
+  clear_error();
+  if (!ctx || !n_cpus) return set_error(HL_EINVAL, "null argument");
+  *n_cpus = (uint32_t)ctx->cpus.size();
+  for (uint32_t i = 0; cpus && i < cap && i < ctx->cpus.size(); ++i) cpus[i] = ctx->cpus[i];
+  return HL_OK;
+}
+
+extern "C" int hl_topology_resolve(const char* pci_bus_id, int32_t requested_node, int32_t* node, int32_t* cpus,
+                                   uint32_t cap, uint32_t* n_cpus) {
+  clear_error();
+  if (!node || !n_cpus) return set_error(HL_EINVAL, "null argument");
+  *node = resolve_node(pci_bus_id, requested_node);
+  const std::vector<int> c = node_cpus(*node);
+  *n_cpus = (uint32_t)c.size();
+  for (uint32_t i = 0; cpus && i < cap && i < c.size(); ++i) cpus[i] = c[i];
+  return HL_OK;
 }
 
 extern "C" int hl_file_residency(const char* path, double* frac) {

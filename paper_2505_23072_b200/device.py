@@ -343,7 +343,8 @@ def transfer_from_file(buf: DeviceBuffer, dev_off: int, file, file_off: int, len
         raise IoError(f"unexpected EOF: [{file_off}, {file_off + length}) past the end of {path}")
     eng = engine_for(buf.device_id, engine_team(), buf.backend.bounce_buffer_bytes, buf.backend.io_mode)
     with torch.cuda.device(buf.device_id):
-        eng.transfer(path, file_off, length, buf.ptr + dev_off)
+        eng.transfer(path, file_off, length, buf.ptr + dev_off,
+                     after_stream=torch.cuda.current_stream(buf.device_id).cuda_stream)
 
 
 def _scratch_rewrite(buf: DeviceBuffer, end: int, descs_into) -> None:

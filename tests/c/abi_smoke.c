@@ -4,7 +4,7 @@
  *
  *   abi_smoke FILE OUT
  *
- * 1. hl_execute_plan: the whole FILE -> one cudaMalloc'd device buffer A
+ * 1. hl_execute_plan_after: the whole FILE -> one cudaMalloc'd device buffer A
  * 2. hl_gather, one launch per kind:
  *      B = A[3 : 3 + nb]               (U8 copy from a misaligned source: realign)
  *      C = bf16 -> f16 of A[16 : 16 + 2*nc]
@@ -53,7 +53,7 @@ int main(int argc, char** argv) {
   const char* paths[1] = {argv[1]};
   hl_block blk = {0, 0, 0, size, (uint64_t)(uintptr_t)a};
   hl_plan_stats stats;
-  CHECK(hl_execute_plan(ctx, paths, 1, &blk, 1, &stats));
+  CHECK(hl_execute_plan_after(ctx, paths, 1, &blk, 1, NULL, &stats));
   printf("landed %llu bytes in %.4f s\n", (unsigned long long)stats.bytes, stats.seconds);
 
   hl_desc d[3];

@@ -45,7 +45,7 @@ def test_struct_sizes_match_header_layout():
 
 def test_version_and_conversion_table():
     lib = _native.load()
-    assert lib.hl_abi_version() == 1 and b"sm_100a" in lib.hl_version()
+    assert lib.hl_abi_version() == 2 and b"sm_100a" in lib.hl_version()
     assert lib.hl_gather_max_batch() >= 256
     for s in range(13):
         for d in range(13):

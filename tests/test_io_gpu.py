@@ -134,3 +134,57 @@ def test_auto_mode_is_per_chunk_hybrid(blob):
         d2 = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
         eng.execute([str(path)], [(0, 0, off, n, d2.data_ptr())])
         assert np.array_equal(d2.cpu().numpy()[:n], data[off:off + n])
+
+
+def test_engine_writes_wait_for_the_callers_stream(blob):
+    """Write-after-read guard (hl_execute_plan_after): a copy queued on the
+    current stream behind a long spin still reads the OLD bytes of a buffer
+    the engine is asked to overwrite right away."""
+    path, data = blob
+    n = 8 << 20
+    eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode="buffered")
+    old = torch.full((n,), 7, dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(old)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(400_000_000)  # ~0.2 s of spinning on the current stream
+    out.copy_(old)  # queued behind the spin
+    eng.execute([str(path)], [(0, 0, 0, n, old.data_ptr())],
+                after_stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert bool((out == 7).all()), "the engine overwrote bytes a queued kernel had not read yet"
+    assert np.array_equal(old.cpu().numpy(), data[:n])
+    eng.close()
+
+
+def test_worker_team_is_persistent_and_pinned(blob):
+    """The engine's team is spawned once per context (no threads per plan)
+    and every team thread runs on the context's CPUs (ref transfer.py:274-293)."""
+    import os
+
+    path, data = blob
+    eng = _native.IoEngine(0, workers=3, chunk_bytes=1 << 20, io_mode="buffered")
+    dst = torch.empty(4 << 20, dtype=torch.uint8, device="cuda")
+
+    def team():
+        out = {}
+        for tid in os.listdir("/proc/self/task"):
+            try:
+                name = open(f"/proc/self/task/{tid}/comm").read().strip()
+            except OSError:
+                continue
+            if name.startswith("hl-io-0-"):
+                out[int(tid)] = os.sched_getaffinity(int(tid))
+        return out
+
+    before = {t for t in team()}
+    eng.execute([str(path)], [(0, 0, 0, 4 << 20, dst.data_ptr())])
+    first = team()
+    eng.execute([str(path)], [(0, 0, 0, 4 << 20, dst.data_ptr())])
+    second = team()
+    new = {t: a for t, a in first.items() if t not in before}
+    assert len(new) == 3 and set(second) == set(first)
+    cpus = eng.cpus()
+    if cpus:
+        assert all(a == set(cpus) for a in new.values())
+    eng.close()
+    assert not set(new) & set(team())  # joined on close

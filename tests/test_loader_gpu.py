@@ -491,3 +491,34 @@ def test_safe_open_and_context_managers(tmp_path, rng):
             v.tobytes()
     # ... while the torch tensor the user holds stays valid (torch owns the memory)
     assert x.reshape(-1).view(torch.uint8).cpu().numpy().tobytes() == t[sorted(t)[0]][2]
+
+
+@pytest.mark.parametrize("batched", [False, True])
+def test_back_to_back_loads_never_overwrite_pending_reads(tmp_path, batched):
+    """The upstream per-file-group pattern — load, retrieve, close, next
+    loader — with the retrievals still queued (behind a spin) when close()
+    returns the file buffer to torch's allocator and the next load reuses
+    that memory at once: every retrieved tensor must still hold the FIRST
+    file's bytes (ref transfer.py:364-378: the reference completes by join)."""
+    n = 6 << 20
+    files = []
+    for i in range(2):
+        raw = np.full(n, 17 + 100 * i, dtype=np.uint8)
+        raw[::4097] = i  # not constant, same size
+        files.append((_write(tmp_path, f"f{i}.safetensors", {"w": (DType.U8, (n,), raw.tobytes())}), raw))
+    loader = SafeTensorsFileLoader(SingleGroup(), "host", config=LoaderConfig(auto_release=True))
+    loader.add_filenames({0: [files[0][0]]})
+    fb = loader.copy_files_to_device()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(400_000_000)  # keep the retrieval below queued for ~0.2 s
+    got = fb.get_tensors(["w"])["w"] if batched else fb.get_tensor("w")
+    fb.close()
+    loader.close()
+    second = SafeTensorsFileLoader(SingleGroup(), "host", config=LoaderConfig(auto_release=False))
+    second.add_filenames({0: [files[1][0]]})
+    fb2 = second.copy_files_to_device()
+    torch.cuda.synchronize()
+    assert np.array_equal(got.torch.cpu().numpy(), files[0][1])
+    assert np.array_equal(fb2.get_tensor("w").torch.cpu().numpy(), files[1][1])
+    fb2.close()
+    second.close()

@@ -2,7 +2,8 @@
 // O_DIRECT reads, (a) T threads of synchronous pread, (b) one io_uring ring at
 // queue depth Q (raw syscalls, no liburing). Prints one JSON line per config.
 //   gcc -O2 -pthread -o /tmp/storage_probe tools/storage_probe.c
-//   /tmp/storage_probe FILE      (drops the file from the page cache before each run)
+//   /tmp/storage_probe FILE [quick]  (drops the file from the page cache before each run;
+//                                     quick: the two configs that measured best, for bench.py)
 #define _GNU_SOURCE
 #include <fcntl.h>
 #include <linux/io_uring.h>
@@ -154,6 +155,11 @@ int main(int argc, char** argv) {
   struct stat st;
   if (stat(g_path, &st)) return 2;
   g_size = (uint64_t)st.st_size & ~4095ull;
+  if (argc > 2 && strcmp(argv[2], "quick") == 0) {
+    threads(64, 4 << 20);
+    uring(64, 1 << 20);
+    return 0;
+  }
   threads(16, 16 << 20);
   threads(32, 4 << 20);
   threads(64, 1 << 20);
