@@ -9,23 +9,28 @@ N(0,0.02) rounded to bf16), 1 x B200, get_tensor for every key with the
 reference's default auto_release=True. The files are generated on the box
 (GPU RNG, written once to --data-dir) before anything is timed.
 At N > 1 the same checkpoint is loaded tensor-parallel: files round-robin to
-ranks, get_sharded with Megatron dims over NCCL, norms replicated
-(strong scaling: the model is fixed as N grows).
+ranks (ref cli.py:286-288), get_sharded with Megatron dims, norms replicated
+(strong scaling: the model is fixed as N grows), on the NCCL data plane
+(ncclBroadcast / grouped send-recv) and on the peer-memory plane.
 
 One JSON line on rank 0:
-  value  — HBM-resident leg: file bytes already landed in HBM, one step makes
-           every tensor ready (auto-release clones through the batched
-           get_tensors, one hl_gather launch) — tensor GB/s, CUDA events.
-  e2e    — the drop-in API end to end from files on disk (page cache warm):
-           SafeTensorsFileLoader.add_filenames -> copy_files_to_device ->
-           get_tensor per key -> synchronize + a D2H read of a result checksum.
-           "e2e_cold" repeats it after dropping the page cache.
-  roofline   — hl_gather: algorithmic bytes (read+write) / launch time vs the
-               measured HBM copy peak (MEASURED_PEAKS.json).
-  io_roofline — measured storage read (O_DIRECT, warm pread) and pinned H2D.
-  cpu_baseline — the reference's CPU pipeline (oracle port) on a bounded
-               sample, on this box's host cores.
---impl reference: that CPU pipeline is the measured arm (rank 0 only).
+  value / ms_per_step — THE metric: files on disk (page cache warm) -> every
+           tensor ready on the device, through the drop-in API
+           (SafeTensorsFileLoader.add_filenames -> copy_files_to_device ->
+           get_tensor / get_sharded per key -> synchronize + a D2H read of a
+           result), GB/s of tensor bytes and seconds to ready; max over ranks.
+  e2e    — the same measurement with its H2D/D2H byte counts and phases.
+  e2e_cold — the same after dropping the page cache (residency checked by
+           mincore right before every cold step), against the storage probe.
+  roofline — the dominant kernel (hl_gather) on the HBM-resident leg: file
+           bytes already landed in HBM, one step makes every tensor ready;
+           algorithmic bytes / CUDA-event launch time vs MEASURED_PEAKS.json.
+  io_roofline — pinned H2D, cold storage (tools/storage_probe.c: O_DIRECT
+           pread threads and io_uring), GDS availability.
+  cpu_baseline — the reference's own CPU loader (baseline/_ref aggload, else
+           the oracle port) on this box's cores, warm and cold.
+--impl reference: that CPU loader is the measured arm (rank 0 only), same
+config dict as this arm.
 """
 
 from __future__ import annotations
@@ -37,6 +42,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 from pathlib import Path
 
@@ -46,6 +52,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "model load GB/s & seconds to ready device tensors"
 SHARE_GPU = os.environ.get("HL_SHARE_GPU") == "1"  # exercise the N>1 code path on a 1-GPU box
 ARCH = "llama2-7b"
+NVLINK_GBS = 900.0  # NVLink 5 per GPU per direction (B200)
 
 
 def parse():
@@ -58,19 +65,32 @@ def parse():
     ap.add_argument("--header", default="aligned", choices=["aligned", "odd"])
     ap.add_argument("--backend", default="host")
     ap.add_argument("--data-dir", default=os.environ.get("HL_BENCH_DIR", "/tmp/hl_bench"))
-    ap.add_argument("--cold", type=int, default=1, help="also time e2e after dropping the page cache")
+    ap.add_argument("--cold-steps", type=int, default=2, help="e2e steps after dropping the page cache (0: none)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
-    ap.add_argument("--quick", action="store_true", help="skip io probes, cpu and library baselines")
-    ap.add_argument("--baselines", type=int, default=1,
+    ap.add_argument("--quick", action="store_true", help="skip io probes, cpu baseline and the fresh-process load")
+    ap.add_argument("--baselines", type=int, default=0,
                     help="also time upstream fastsafetensors and safetensors on the same files (N=1)")
     ap.add_argument("--files", type=int, default=0,
                     help="re-split the checkpoint into this many files (0: HF split at N=1, N files at N>1)")
     ap.add_argument("--layers", type=int, default=None,
                     help="keep only the first N transformer blocks (configs larger than one GPU / the disk)")
     ap.add_argument("--cast", default=None, help="on-device dtype conversion at retrieval, e.g. F16 (C5)")
-    ap.add_argument("--data-plane", default="auto", choices=["auto", "ipc", "nccl"],
-                    help="N>1: peer-memory pulls (one hl_gather per rank over NVLink) or NCCL broadcast/scatter")
+    ap.add_argument("--data-plane", default="both", choices=["both", "auto", "ipc", "nccl"],
+                    help="N>1: NCCL broadcast/scatter (value) and peer-memory pulls, or one of them")
+    ap.add_argument("--io-mode", default=None, help="engine I/O mode (auto|buffered|direct|mmap|cufile)")
     return ap.parse_args()
+
+
+def make_config(args, world: int, workload: str, tensor_bytes: int, file_bytes: int, job_bytes: int,
+                n_tensors: int, n_files: int, cast) -> dict:
+    """The workload description both arms print, byte for byte."""
+    return {"workload": workload, "cast": cast.value if cast else None, "layers": args.layers,
+            "tensor_bytes": tensor_bytes, "file_bytes": file_bytes, "ready_bytes_job": job_bytes,
+            "tensors": n_tensors, "files": n_files, "header": args.header, "auto_release": True,
+            "global_batch": 1, "seq_len": 0, "parallelism": f"tp{world}" if world > 1 else "single",
+            "retrieval": "get_tensor per key" if world == 1 else "get_sharded (Megatron dims) / get_tensor per key",
+            "page_cache": "warm for value; cold leg after posix_fadvise(DONTNEED) + drop_caches",
+            "l2": f"inputs ({tensor_bytes / 1e9:.1f} GB) far exceed the 126 MB L2; no flush needed"}
 
 
 # ----------------------------------------------------------------------------- data
@@ -150,12 +170,65 @@ def warm_cache(paths, threads: int = 16, chunk: int = 64 << 20) -> None:
         t.join()
 
 
-def residency(paths) -> float:
-    """Byte-weighted page-cache residency of the files (mincore)."""
-    from paper_2505_23072_b200 import _native
+_libc = None
 
+
+def _file_residency(path) -> float:
+    """Fraction of the file's pages in the page cache (mincore through libc;
+    no project code, so both bench arms use it)."""
+    import ctypes
+
+    global _libc
+    if _libc is None:
+        _libc = ctypes.CDLL(None, use_errno=True)
+        _libc.mmap.restype = ctypes.c_void_p
+        _libc.mmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_long]
+        _libc.munmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        _libc.mincore.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    size = os.path.getsize(path)
+    if size == 0:
+        return 1.0
+    fd = os.open(str(path), os.O_RDONLY)
+    try:
+        addr = _libc.mmap(None, size, 1, 1, fd, 0)  # PROT_READ, MAP_SHARED
+        if addr in (None, ctypes.c_void_p(-1).value):
+            return 0.0
+        pages = (size + 4095) // 4096
+        vec = (ctypes.c_ubyte * pages)()
+        ok = _libc.mincore(addr, size, vec) == 0
+        _libc.munmap(addr, size)
+        return sum(v & 1 for v in bytes(vec)) / pages if ok else 0.0
+    finally:
+        os.close(fd)
+
+
+def residency(paths) -> float:
+    """Byte-weighted page-cache residency of the files."""
     sizes = [os.path.getsize(p) for p in paths]
-    return round(sum(_native.file_residency(str(p)) * n for p, n in zip(paths, sizes)) / max(sum(sizes), 1), 4)
+    return round(sum(_file_residency(p) * n for p, n in zip(paths, sizes)) / max(sum(sizes), 1), 4)
+
+
+def drop_cache(paths) -> float:
+    """The reference's cold pass (ref cli.py:177-186: posix_fadvise DONTNEED per
+    file), plus a system-wide drop when permitted (root on the box). Returns
+    the residency measured right after (byte-weighted)."""
+    for p in paths:
+        fd = os.open(str(p), os.O_RDONLY)
+        try:
+            os.fdatasync(fd)
+            os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+        finally:
+            os.close(fd)
+    r = residency(paths)
+    if r > 0.0:
+        try:
+            with open("/proc/sys/vm/drop_caches", "w") as f:
+                f.write("1\n")
+        except OSError:
+            pass
+        r = residency(paths)
+    return r
 
 
 def host_memory() -> dict:
@@ -169,18 +242,6 @@ def host_memory() -> dict:
     except OSError:
         pass
     return out
-
-
-def drop_cache(paths):
-    from paper_2505_23072_b200 import _native
-
-    for p in paths:
-        _native.drop_cache(str(p))
-    try:  # system-wide drop when permitted (root on the box)
-        with open("/proc/sys/vm/drop_caches", "w") as f:
-            f.write("1\n")
-    except OSError:
-        pass
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -226,77 +287,157 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def run_cpu_reference(paths, steps: int, warmup: int, world: int = 1, policy=None, cast=None):
-    """The reference's CPU load pipeline (oracle port of aggload's loader) on
-    the FULL workload of this arm: W thread-ranks (the reference's in-process
-    ProcessGroup), files round-robin to ranks, each rank's thread-rule preadv
-    workers land its files (transfer.py:197-201, 305-389), then every rank
-    retrieves every key — an auto-release clone (loader.py:456-461) or its
-    slice along the Megatron dim (collective.py:318-330) — from the owner's
-    host buffer. ``cast``: the reference's loader cannot convert (SURVEY
-    §8a a7), so its conversion (device.convert_dtype = numpy astype) is applied
-    to each retrieved tensor. Returns ready tensor bytes per second over all ranks."""
-    import threading
+def reference_package():
+    """The unmodified reference (pkg/src/aggload) installed under baseline/_ref
+    (pip --target), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "aggload" / "__init__.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import aggload
+    except Exception:  # noqa: BLE001 - fall back to the port
+        return None
+    return aggload
 
+
+def _reference_pass(agg, mapping, keys, policy, world: int, cast) -> int:
+    """One load through the reference's public API the way its bench does
+    (ref cli.py:201-263): W thread-ranks in one ProcessGroup, every rank
+    add_filenames -> copy_files_to_device -> get_sharded / get_tensor per key.
+    The reference cannot convert at retrieval, so a cast
+    applies its own element conversion (ref device.py:310-320) to each
+    retrieved tensor. Returns the ready bytes over all ranks."""
+    from aggload.device import _convert_elements
+
+    group = agg.ProcessGroup(world)
+    got = [0] * world
+    errors = []
+    dst = agg.DType(cast.value) if cast is not None else None
+
+    def rank_main(r):
+        try:
+            loader = agg.SafeTensorsFileLoader(group, rank=r, config=agg.LoaderConfig(auto_release=True))
+            loader.add_filenames(mapping)
+            fb = loader.copy_files_to_device()
+            nb = 0
+            for k in keys:
+                d = policy.get(k) if world > 1 else None
+                v = fb.get_tensor(k) if d is None else fb.get_sharded(k, d)
+                if dst is not None and v.dtype is not dst:
+                    raw = v.buffer.array[v.base_offset:v.base_offset + v.nbytes]
+                    nb += _convert_elements(raw, v.dtype, dst).nbytes
+                else:
+                    nb += v.nbytes
+            fb.close()
+            loader.close()
+            got[r] = nb
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+            group.abort(f"rank {r} failed: {type(e).__name__}: {e}")
+
+    ts = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errors:
+        raise errors[0]
+    return sum(got)
+
+
+def _port_pass(mapping, keys, policy, world: int, cast) -> int:
+    """The same pass through the oracle port (oracle.CpuLoader), used only
+    when baseline/_ref is absent."""
     from oracle import oracle
 
-    mapping = {r: [p for i, p in enumerate(paths) if i % world == r] for r in range(world)}
-    workers = {r: oracle.thread_rule(len(mapping[r])) for r in range(world)}
-    policy = policy or {}
+    loaders = {r: oracle.CpuLoader(mapping[r], workers=oracle.thread_rule(len(mapping[r])))
+               for r in range(world) if mapping[r]}
+    ts = [threading.Thread(target=ld.copy) for ld in loaders.values()]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    owner = {k: ld for ld in loaders.values() for k in ld.index}
+    got = [0] * world
+    meet = threading.Barrier(world) if world > 1 else None
+    tag = cast.value if cast is not None else None
+
+    def retrieve(r):
+        nb = 0
+        for k in keys:
+            ld = owner[k]
+            d = policy.get(k) if world > 1 else None
+            if meet:
+                meet.wait()
+            nb += (ld.get_tensor(k, tag) if d is None else ld.get_sharded(k, d, world, r, tag)).nbytes
+            if meet:
+                meet.wait()
+        got[r] = nb
+
+    ts = [threading.Thread(target=retrieve, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return sum(got)
+
+
+def run_cpu_reference(paths, keys, policy, steps: int, warmup: int, cold_steps: int, world: int = 1,
+                      cast=None) -> dict:
+    """The reference's CPU load path on this box's host cores, warm page cache
+    (median of ``steps`` after ``warmup``) and cold (``cold_steps`` passes, each
+    after the reference's own cache drop, ref cli.py:177-186, 291-294, with the
+    residency measured right before). Returns ready tensor bytes/s over all ranks."""
+    agg = reference_package()
+    kind = "reference" if agg is not None else "port"
+    mapping = {r: [str(p) for i, p in enumerate(paths) if i % world == r] for r in range(world)}
+
+    def one():
+        t0 = time.perf_counter()
+        n = _reference_pass(agg, mapping, keys, policy, world, cast) if agg is not None else \
+            _port_pass(mapping, keys, policy, world, cast)
+        return time.perf_counter() - t0, n
+
+    warm_cache(paths)
     times, ready = [], 0
     for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        loaders = {r: oracle.CpuLoader(mapping[r], workers=workers[r]) for r in range(world) if mapping[r]}
-        ts = [threading.Thread(target=ld.copy) for ld in loaders.values()]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-        owner = {k: ld for ld in loaders.values() for k in ld.index}
-        got = [0] * world
-        # the reference's broadcast / scatter rendezvous twice per key (the data
-        # exchange and the "done" exchange, collective.py:175-255)
-        meet = threading.Barrier(world) if world > 1 else None
-
-        def retrieve(r):
-            nb = 0
-            for k, ld in owner.items():
-                d = policy.get(k) if world > 1 else None
-                tag = cast.value if cast is not None else None
-                if meet:
-                    meet.wait()
-                nb += (ld.get_tensor(k, tag) if d is None else ld.get_sharded(k, d, world, r, tag)).nbytes
-                if meet:
-                    meet.wait()
-            got[r] = nb
-
-        ts = [threading.Thread(target=retrieve, args=(r,)) for r in range(world)]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-        dt = time.perf_counter() - t0
-        del loaders, owner
-        ready = sum(got)
+        dt, ready = one()
         if i >= warmup:
             times.append(dt)
     t = statistics.median(times)
-    threads = max(sum(workers.values()), world)
-    return {"value": ready / t / 1e9, "unit": "GB/s", "cores": threads, "kind": "port", "seconds": t,
-            "sample": f"full workload: {len(paths)} file(s), {ready} ready tensor bytes over {world} rank(s), warm "
-                      f"page cache; reference thread rule per rank ({sorted(set(workers.values()))} preadv "
-                      f"worker(s)), then {world} retrieval thread(s) meeting twice per key (auto-release clones"
-                      + (" / Megatron-dim slices" if world > 1 else "")
-                      + (f", numpy {cast.value} conversion" if cast is not None else "")
-                      + f"); host os.cpu_count()={os.cpu_count()}"}
+    cold, resid = [], []
+    for _ in range(cold_steps):
+        resid.append(drop_cache(paths))
+        cold.append(one()[0])
+    if cold_steps:
+        warm_cache(paths)  # leave the files warm for whatever runs next
+    from oracle import oracle  # the thread rule only (ref transfer.py:197-201)
+
+    readers = sum(oracle.thread_rule(len(m)) for m in mapping.values() if m)
+    threads = readers + (world if world > 1 else 0)
+    out = {"value": round(ready / t / 1e9, 4), "unit": "GB/s", "seconds": round(t, 4), "kind": kind,
+           "host_cores": os.cpu_count(), "threads": threads, "cores": threads,
+           "sample": (f"full workload, {len(paths)} file(s), {ready} ready bytes over {world} thread-rank(s); "
+                      f"{'aggload ' + getattr(agg, '__version__', '?') + ' from baseline/_ref' if agg else 'oracle port'}"
+                      f", reference thread rule: {readers} preadv reader(s)"
+                      + (f", {world} retrieval threads" if world > 1 else "")
+                      + (f", element conversion to {cast.value}" if cast is not None else "")
+                      + f"; host os.cpu_count()={os.cpu_count()}")}
+    if cold_steps:
+        tc = statistics.median(cold)
+        out["cold"] = {"value": round(ready / tc / 1e9, 4), "unit": "GB/s", "seconds": round(tc, 4),
+                       "residency_before": resid, "steps": cold_steps}
+    return out
 
 
 # ----------------------------------------------------------------------------- io probes
-def io_probes(paths, device_index: int):
-    """Measured I/O roofline terms: pinned H2D, warm buffered read, cold O_DIRECT read."""
+def io_probes(paths, device_index: int) -> dict:
+    """Measured I/O roofline terms: pinned H2D (CUDA events) and cold storage
+    reads (tools/storage_probe.c: 64 O_DIRECT pread threads and one io_uring
+    at depth 64, file dropped from the page cache before each)."""
     import torch
-
-    from paper_2505_23072_b200 import _native
 
     out = {}
     n = 1 << 30
@@ -311,64 +452,29 @@ def io_probes(paths, device_index: int):
         d.copy_(h, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
-    out["h2d_gbs"] = 4 * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+    out["h2d_gbs"] = round(4 * n / (e0.elapsed_time(e1) / 1e3) / 1e9, 3)
     del h, d
-    big = paths[0]
-    size = os.path.getsize(big)
-    dev = torch.empty(size, dtype=torch.uint8, device=f"cuda:{device_index}")
-    for mode in ("buffered", "direct"):
-        eng = _native.IoEngine(device_index, io_mode=mode)
-        if mode == "direct":
-            _native.drop_cache(str(big))
-        st = eng.execute([str(big)], [(0, 0, 0, size, dev.data_ptr())])
-        if mode == "buffered":  # second pass: fully warm
-            st = eng.execute([str(big)], [(0, 0, 0, size, dev.data_ptr())])
-        out[f"{mode}_read_to_hbm_gbs"] = size / st["seconds"] / 1e9
-        eng.close()
-    del dev
-    # storage-only read rate (no GPU in the loop): O_DIRECT, 16 threads
-    _native.drop_cache(str(big))
-    out["storage_direct_read_gbs"] = _storage_read(big)
+    probe = ROOT / "tools" / "build" / "storage_probe"
+    big = max(paths, key=os.path.getsize)
+    if probe.exists():
+        try:
+            r = subprocess.run([str(probe), str(big), "quick"], capture_output=True, text=True, timeout=300)
+            rows = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+            out["storage_probe"] = rows
+            best = [x["GBps"] for x in rows if "GBps" in x]
+            out["storage_gbs"] = round(max(best), 3) if best else None
+        except Exception as e:  # noqa: BLE001 - reported
+            out["storage_probe"] = f"{type(e).__name__}: {e}"[:200]
+    else:
+        out["storage_probe"] = "tools/build/storage_probe not built"
+    warm_cache([big])
     return out
-
-
-def _storage_read(path, threads: int = 16, chunk: int = 16 << 20) -> float:
-    import mmap
-    import threading
-
-    size = os.path.getsize(path)
-    fd = os.open(str(path), os.O_RDONLY | os.O_DIRECT)
-    cursor = [0]
-    lock = threading.Lock()
-
-    def work():
-        buf = mmap.mmap(-1, chunk)
-        while True:
-            with lock:
-                off = cursor[0]
-                cursor[0] += chunk
-            if off >= size:
-                break
-            os.preadv(fd, [buf], off)
-        buf.close()
-
-    t0 = time.perf_counter()
-    ts = [threading.Thread(target=work) for _ in range(threads)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    dt = time.perf_counter() - t0
-    os.close(fd)
-    return size / dt / 1e9
 
 
 def library_baselines(paths, device_index: int, tensor_bytes: int, steps: int = 3) -> dict:
     """Same files, same box, warm page cache, every key ready on the GPU
-    (median of ``steps`` after one warm-up): the paper's own implementation
-    (upstream fastsafetensors 0.3.1 from the image, GDS off since the box has
-    no nvidia-fs: its pread + bounce-buffer path; get_tensor returns views)
-    and the paper's baseline (safetensors ``load_file(device="cuda")``)."""
+    (median of ``steps`` after one warm-up): upstream fastsafetensors 0.3.1
+    from the image (GDS off: no nvidia-fs) and safetensors load_file."""
     import torch
 
     dev = f"cuda:{device_index}"
@@ -438,9 +544,9 @@ print(json.dumps({{"seconds": time.perf_counter() - t0}}))
 
 
 def e2e_fresh_process(paths, device_index: int, backend: str, job_bytes: int) -> dict | None:
-    """The same e2e load as the FIRST load of a fresh process (what a model
-    server pays once: engine threads, pinned ring, allocator growth, kernel
-    module loading), CUDA context creation excluded; warm page cache."""
+    """The same e2e load as the FIRST load of a fresh process (engine threads,
+    pinned ring, allocator growth, kernel module loading), CUDA context
+    creation excluded; warm page cache."""
     code = FRESH.format(root=str(ROOT), dev=device_index, backend=backend, paths=[str(p) for p in paths])
     try:
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
@@ -462,6 +568,22 @@ def hbm_peak_gbs() -> tuple[float, str]:
 
 
 # ----------------------------------------------------------------------------- GPU legs
+def output_checksum(outs) -> int:
+    """Order-weighted sum of every output's 16-bit words (int64 wrap-around):
+    identical bytes on two data planes give identical sums."""
+    import torch
+
+    acc = 0
+    for i, v in enumerate(outs):
+        t = v.torch.reshape(-1).view(torch.uint8)
+        n = t.numel()
+        s = int(t[: n - n % 2].view(torch.int16).sum(dtype=torch.int64).item()) if n >= 2 else 0
+        if n % 2:
+            s += int(t[-1].item())
+        acc = (acc + (i + 1) * s) & ((1 << 62) - 1)
+    return acc
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -471,7 +593,9 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        if SHARE_GPU:  # test mode: every rank on cuda:0, gloo control plane (NCCL refuses shared GPUs)
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        elif SHARE_GPU:  # test mode: every rank on cuda:0, gloo control plane (NCCL refuses shared GPUs)
             local = 0
             torch.cuda.set_device(0)
             dist.init_process_group("gloo")
@@ -482,11 +606,11 @@ def main():
     hf_files = len(synth_split(args.arch, args.layers))
     n_files = args.files if args.files else (None if world <= hf_files else world)
     paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist, n_files, args.layers)
-    from paper_2505_23072_b200 import synth
-
+    from paper_2505_23072_b200 import kernels, synth
     from paper_2505_23072_b200.format import DType
 
     ents = synth.entries(args.arch, args.layers)
+    keys = [e[0] for e in ents]
     tensor_bytes = sum(synth.nbytes(e) for e in ents)
     cast = DType.from_tag(args.cast.upper()) if args.cast else None
     src_dt = ents[0][1]
@@ -496,46 +620,7 @@ def main():
                 + ("get_tensor every key" if world == 1 else f"TP={world} get_sharded (Megatron dims)")
                 + (f", on-device {src_dt.value}->{cast.value} cast" if cast else ""))
     file_bytes = sum(os.path.getsize(p) for p in paths)
-
-    if args.impl == "reference":
-        if rank == 0:
-            policy = {e[0]: synth.shard_dim(e[0], e[2]) for e in ents}
-            r = run_cpu_reference(paths, args.steps, max(args.warmup, 1), world, policy, cast)
-            line = {"metric": METRIC, "value": round(r["value"], 4), "unit": "GB/s", "n_gpus": args.gpus,
-                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["seconds"] * 1e3, 1),
-                    "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag,
-                    "data": "synthetic", "impl": "reference",
-                    "config": {"workload": workload, "global_batch": 1, "seq_len": 0, "parallelism": f"cpu, {world} thread-rank(s)"},
-                    "cpu_baseline": r,
-                    "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                            "d2h_bytes_per_step": 0}}
-            print(json.dumps(line), flush=True)
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader, SingleGroup, _native, kernels
-    from paper_2505_23072_b200.loader import FilesBufferOnDevice, _HostedFile
-    from paper_2505_23072_b200.device import DeviceBuffer
-
-    device = torch.device("cuda", local)
-    torch.cuda.set_device(device)
-    group = DistGroup(device=device, data_plane=args.data_plane) if world > 1 else SingleGroup()
-    mapping = {r: [str(p) for i, p in enumerate(paths) if i % world == r] for r in range(world)}
-    keys = [e[0] for e in ents]
     policy = {e[0]: (synth.shard_dim(e[0], e[2]) if world > 1 else None) for e in ents}
-    cfg = LoaderConfig(backend=args.backend, auto_release=True)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     def ready_bytes_for_rank(r: int, out: bool = False) -> int:
         """Tensor body bytes rank r makes ready (its slices of sharded keys);
@@ -551,8 +636,81 @@ def main():
                 nb += math.prod(shape) // shape[d] * (hi - lo) * osz
         return nb
 
-    job_bytes = sum(ready_bytes_for_rank(r) for r in range(world))  # the metric: Σ tensor body bytes
-    out_bytes = sum(ready_bytes_for_rank(r, out=True) for r in range(world))
+    job_bytes = sum(ready_bytes_for_rank(r) for r in range(world))  # the metric: sum of tensor body bytes
+    config = make_config(args, world, workload, tensor_bytes, file_bytes, job_bytes, len(ents), len(paths), cast)
+
+    if args.impl == "reference":
+        if rank == 0:
+            r = run_cpu_reference(paths, keys, policy, args.steps, max(args.warmup, 1), args.cold_steps, world, cast)
+            line = {"metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["seconds"] * 1e3, 1),
+                    "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag,
+                    "data": "synthetic", "impl": "reference", "config": config,
+                    "engine": {"backend": "host (reference: numpy host buffers)", "threads": r["threads"],
+                               "host_cores": r["host_cores"]},
+                    "cpu_baseline": r,
+                    "e2e": {"value": r["value"], "unit": "GB/s", "seconds_to_ready": r["seconds"],
+                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0, "page_cache": "warm"},
+                    "e2e_cold": r.get("cold")}
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    from paper_2505_23072_b200 import DistGroup, LoaderConfig, SafeTensorsFileLoader, SingleGroup, _native
+    from paper_2505_23072_b200.device import DeviceBuffer
+    from paper_2505_23072_b200.loader import FilesBufferOnDevice, _HostedFile
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        planes = ["nccl", "ipc"] if args.data_plane == "both" else [args.data_plane]
+        groups = {p: DistGroup(device=device, data_plane=p) for p in planes}
+        # the NCCL plane carries `value` (north_star: NCCL broadcast/scatter); ipc beside it
+        group = groups[planes[0]]
+    else:
+        groups = {"single": SingleGroup()}
+        group = groups["single"]
+    mapping = {r: [str(p) for i, p in enumerate(paths) if i % world == r] for r in range(world)}
+    cfg = LoaderConfig(backend=args.backend, auto_release=True, io_mode=args.io_mode)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_ranks(x):
+        if world == 1:
+            return [x]
+        out = [None] * world
+        dist.all_gather_object(out, x)
+        return out
+
+    # bytes each rank receives from other ranks' files (the link traffic of one load)
+    my_files = set(mapping[rank])
+    owner_file = {}
+    for p in paths:
+        from paper_2505_23072_b200.format import read_header
+
+        for k in read_header(str(p)).tensors:
+            owner_file[k] = str(p)
+    recv_bytes = 0
+    for name, dt, shape in ents:
+        if owner_file[name] in my_files:
+            continue
+        d = policy[name]
+        osz = (cast or dt).size_bytes
+        if d is None:
+            recv_bytes += math.prod(shape) * osz
+        else:
+            lo, hi = kernels.shard_bounds(shape[d], world, rank)
+            recv_bytes += math.prod(shape) // shape[d] * (hi - lo) * osz
 
     dims = {k: d for k, d in policy.items() if d is not None}
 
@@ -565,8 +723,9 @@ def main():
             outs.append(fb.get_tensor(k, dtype=cast) if d is None else fb.get_sharded(k, d, dtype=cast))
         return outs
 
-    # ---- value leg: landed bytes in HBM -> ready tensors --------------------------------
-    base_loader = SafeTensorsFileLoader(group, args.backend, rank=rank,
+    # ---- roofline leg: landed bytes in HBM -> ready tensors (dominant kernel) -------------
+    hbm_group = groups.get("ipc", group) if world > 1 else group
+    base_loader = SafeTensorsFileLoader(hbm_group, args.backend, rank=rank,
                                         config=LoaderConfig(backend=args.backend, auto_release=False))
     base_loader.add_filenames(mapping)
     landed = base_loader.copy_files_to_device()
@@ -584,7 +743,7 @@ def main():
         return fb
 
     kernels.TIMING = []
-    vals, dom_ms, dom_bytes = [], [], 0
+    vals, dom_ms, dom_bytes, k_ms, k_bytes, k_n = [], [], 0, 0.0, 0, 0
     launches_value = 0
     for i in range(args.warmup + args.steps):
         fb = fresh_fb()
@@ -614,8 +773,7 @@ def main():
         fb._hosted, fb._peer = {}, None  # landed buffers (and their mappings) are shared across steps
         fb.close()
     kernels.TIMING = None
-    value_ms = statistics.median(vals)
-    value = job_bytes / (value_ms / 1e3) / 1e9
+    value_leg_ms = statistics.median(vals)
     hbm_peak, peak_source = hbm_peak_gbs()
     achieved = dom_bytes / (statistics.mean(dom_ms) / 1e3) / 1e9 if dom_ms else None
     achieved_all = k_bytes / (k_ms / 1e3) / 1e9 if k_n else None
@@ -633,138 +791,160 @@ def main():
     base_loader.close()
     torch.cuda.empty_cache()
 
-    # ---- e2e leg: files on disk -> ready tensors through the drop-in API ------------------
-    def e2e_step():
+    # ---- the metric: files on disk -> ready tensors through the drop-in API ----------------
+    def e2e_step(g, record=None, checksum=False):
         barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1, er = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         t0 = time.perf_counter()
         e0.record()
-        loader = SafeTensorsFileLoader(group, args.backend, rank=rank, config=cfg)
+        loader = SafeTensorsFileLoader(g, args.backend, rank=rank, config=cfg)
         loader.add_filenames(mapping)
         t1 = time.perf_counter()
         fb = loader.copy_files_to_device()
+        er.record()
         t2 = time.perf_counter()
         outs = retrieve(fb, batched=False)
         t3 = time.perf_counter()
-        checksum = outs[-1].torch.reshape(-1)[:32].view(torch.uint8).cpu()  # D2H read of the result
+        tail = outs[-1].torch.reshape(-1)[:32].view(torch.uint8).cpu()  # D2H read of a result
         e1.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         ms = max(e0.elapsed_time(e1), wall * 1e3)
         stats = loader.last_transfer_stats
-        d2h = checksum.numel()
-        phases.append({"add_filenames_ms": (t1 - t0) * 1e3, "copy_files_to_device_ms": (t2 - t1) * 1e3,
-                       "engine_ms": stats.engine_seconds * 1e3 if stats else 0.0,
-                       "worker_read_s": stats.read_seconds if stats else 0.0,
-                       "worker_wait_s": stats.wait_seconds if stats else 0.0,
-                       "retrieve_enqueue_ms": (t3 - t2) * 1e3, "drain_ms": wall * 1e3 - (t3 - t0) * 1e3})
+        retrieve_ms = er.elapsed_time(e1)
+        if record is not None:
+            record.append({"add_filenames_ms": (t1 - t0) * 1e3, "copy_files_to_device_ms": (t2 - t1) * 1e3,
+                           "engine_ms": stats.engine_seconds * 1e3 if stats else 0.0,
+                           "worker_read_s": stats.read_seconds if stats else 0.0,
+                           "worker_wait_s": stats.wait_seconds if stats else 0.0,
+                           "retrieve_enqueue_ms": (t3 - t2) * 1e3, "retrieve_gpu_ms": retrieve_ms,
+                           "drain_ms": wall * 1e3 - (t3 - t0) * 1e3})
+        csum = output_checksum(outs) if checksum else None
         del outs
         fb.close()
         loader.close()
-        return max_over_ranks(ms), stats, d2h
+        return max_over_ranks(ms), stats, tail.numel(), max_over_ranks(retrieve_ms), csum
 
-    phases = []
+    def run_plane(g, label, clocks=None):
+        phases = []
+        e2e_ms, launches, io_modes, h2d, first_ms, csum = [], 0, set(), 0, None, None
+        warm_cache(mapping[rank])  # "warm" means resident: O_DIRECT reads of a cold file would not make it so
+        resid = residency(mapping[rank])
+        for i in range(args.warmup):
+            ms, _, _, _, c = e2e_step(g, checksum=(i == args.warmup - 1))
+            if c is not None:
+                csum = c
+            if first_ms is None:
+                first_ms = ms
+        if clocks:
+            clocks.start()
+        ret_ms = []
+        st = None
+        d2h = 0
+        for i in range(args.steps):
+            l0 = _native.kernel_launches()
+            ms, st, d2h, rms, _ = e2e_step(g, record=phases)
+            e2e_ms.append(ms)
+            ret_ms.append(rms)
+            launches += _native.kernel_launches() - l0
+            if st is not None:
+                io_modes.update(st.io_modes)
+                h2d = st.bytes
+        clk = clocks.stop() if clocks else None
+        med = statistics.median(e2e_ms)
+        out = {"value": round(job_bytes / (med / 1e3) / 1e9, 3), "unit": "GB/s", "seconds_to_ready": round(med / 1e3, 4),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "page_cache": "warm",
+               "io_modes": sorted(io_modes), "page_cache_residency_before": resid,
+               "first_load_seconds_in_process": round(first_ms / 1e3, 4) if first_ms else None,
+               "phases_ms": {k: round(statistics.median(p[k] for p in phases), 2) for k in phases[-1]},
+               "numa": {"node": st.numa_node, "cpus": len(st.numa_cpus), "io_threads": st.io_threads} if st else None}
+        if world > 1:
+            rm = statistics.median(ret_ms)
+            link = max(gather_ranks(recv_bytes))
+            out.update({"data_plane": label, "link_recv_bytes_per_gpu_max": link,
+                        "retrieve_ms": round(rm, 3),
+                        "link_gbs_per_gpu": round(link / (rm / 1e3) / 1e9, 2) if rm > 0 else None,
+                        "link_frac_of_nvlink": round(link / (rm / 1e3) / 1e9 / NVLINK_GBS, 4) if rm > 0 else None,
+                        "output_checksums": gather_ranks(csum)})
+        return out, med, launches, clk
+
     clocks = Clocks(local)
-    e2e_ms, launches_e2e, io_modes, h2d_bytes, ring = [], 0, set(), 0, 0.0
-    first_ms = None
-    warm_cache(mapping[rank])  # "warm" means resident: O_DIRECT reads of a cold file would not make it so
-    host_mem = host_memory()
-    resid = {"after_warm": residency(mapping[rank])}
-    for i in range(args.warmup):
-        ms, _, _ = e2e_step()
-        if first_ms is None:
-            first_ms = ms  # includes the engine's one-time pinned-ring setup and CUDA lazy init
-    clocks.start()
-    for i in range(args.steps):
-        l0 = _native.kernel_launches()
-        ms, st, d2h = e2e_step()
-        e2e_ms.append(ms)
-        launches_e2e += _native.kernel_launches() - l0
-        if st is not None:
-            io_modes.update(st.io_modes)
-            h2d_bytes = st.bytes
-            ring = max(ring, st.ring_setup_seconds)
-    clk = clocks.stop()
-    resid["after_warm_steps"] = residency(mapping[rank])
-    phase_med = {k: round(statistics.median(p[k] for p in phases[-args.steps:]), 2) for k in phases[-1]}
-    e2e_med = statistics.median(e2e_ms)
-    e2e_val = job_bytes / (e2e_med / 1e3) / 1e9
+    plane_out = {}
+    primary = None
+    for label, g in groups.items():
+        res, med, launches, clk = run_plane(g, label, clocks if primary is None else None)
+        plane_out[label] = res
+        if primary is None:
+            primary = (res, med, launches, clk)
+    e2e, e2e_med, launches_e2e, clk = primary
+    value = job_bytes / (e2e_med / 1e3) / 1e9
 
     cold = None
-    if args.cold:
-        cms = []
-        for i in range(max(1, min(args.steps, 2))):
-            drop_cache(paths)
-            ms, st, _ = e2e_step()
+    if args.cold_steps:
+        cms, resid_before, st = [], [], None
+        for _ in range(args.cold_steps):
+            barrier()
+            resid_before.append(max(gather_ranks(drop_cache(mapping[rank]))))
+            ms, st, _, _, _ = e2e_step(group)
             cms.append(ms)
-        cold = {"value": round(job_bytes / (statistics.median(cms) / 1e3) / 1e9, 3), "unit": "GB/s",
-                "seconds_to_ready": round(statistics.median(cms) / 1e3, 3),
-                "io_modes": sorted(st.io_modes) if st else None}
+        med = statistics.median(cms)
+        cold = {"value": round(job_bytes / (med / 1e3) / 1e9, 3), "unit": "GB/s",
+                "seconds_to_ready": round(med / 1e3, 3), "steps": args.cold_steps,
+                "residency_before": resid_before,
+                "io_modes": sorted(st.io_modes) if st else None,
+                "direct_bytes": st.direct_bytes if st else None,
+                "buffered_bytes": st.buffered_bytes if st else None}
+        warm_cache(mapping[rank])
 
-    io = None
-    cpu = None
-    libs = None
-    views = None
-    fresh = None
+    io = cpu = libs = fresh = None
     if rank == 0 and world == 1 and not args.quick:
-        if args.baselines and cast is None:
-            # apples to apples with upstream (whose get_tensor returns views): our zero-copy mode
-            cfg.auto_release = False
-            warm_cache(paths)  # the cold leg left the files out of the page cache
-            e2e_step()
-            vms = [e2e_step()[0] for _ in range(args.steps)]
-            cfg.auto_release = True
-            views = {"value": round(job_bytes / (statistics.median(vms) / 1e3) / 1e9, 3), "unit": "GB/s",
-                     "seconds_to_ready": round(statistics.median(vms) / 1e3, 4), "auto_release": False}
-            libs = library_baselines(paths, local, tensor_bytes)
-        warm_cache(paths)
         fresh = e2e_fresh_process(paths, local, args.backend, job_bytes) if cast is None else None
+        if args.baselines:
+            libs = library_baselines(paths, local, tensor_bytes)
         if args.cpu_baseline:
-            if not args.baselines:
-                warm_cache(paths)
-            cpu = run_cpu_reference(paths, steps=1, warmup=0, cast=cast)  # warm page cache, like the e2e leg
-        io = io_probes(paths, local)  # last: it drops the first file from the page cache
-
+            cpu = run_cpu_reference(paths, keys, policy, steps=1, warmup=0, cold_steps=1 if args.cold_steps else 0,
+                                    cast=cast)
+        io = io_probes(paths, local)
+        io["e2e_frac_of_h2d"] = round(value / io["h2d_gbs"], 4)
+        if cold and io.get("storage_gbs"):
+            io["cold_frac_of_storage"] = round(cold["value"] / io["storage_gbs"], 4)
+            cold["frac_of_storage"] = io["cold_frac_of_storage"]
     if rank == 0:
+        gds = _native.gds_available()
         roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm_peak,
                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4) if achieved else None,
                     "traffic": traffic,
                     "kernel": (f"hl_gather staged_kernel<{src_dt.value}->{cast.value}> (TMA in + out)" if cast
                                else "hl_gather bulk_kernel (TMA cp.async.bulk copy)"),
+                    "leg": "HBM-resident: file bytes already landed, get_tensors makes every key ready",
+                    "value_leg_gbs": round(job_bytes / (value_leg_ms / 1e3) / 1e9, 2),
+                    "value_leg_ms": round(value_leg_ms, 3),
                     "launches_per_step": k_n, "algorithmic_bytes_per_launch": dom_bytes,
                     "achieved_all_launches_of_step": round(achieved_all, 1) if achieved_all else None,
-                    # live: the kernel's share of the value step (the rest is host pre-launch work);
-                    # ncu's launch list has this launch as the step's only GPU work (profiles/)
-                    "kernel_share_of_step": round(k_ms / max(value_ms, 1e-9), 4) if k_n else None,
+                    "kernel_share_of_step": round(k_ms / max(value_leg_ms, 1e-9), 4) if k_n else None,
+                    "launches_value_leg": launches_value,
                     "peak_source": peak_source}
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(value_ms, 3), "higher_is_better": True,
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(e2e_med, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": dtype_tag, "data": "synthetic",
-            "config": {"workload": workload, "cast": cast.value if cast else None,
-                       "layers": args.layers, "tensor_bytes": tensor_bytes, "file_bytes": file_bytes, "ready_bytes_job": job_bytes, "ready_bytes_out": out_bytes,
-                       "tensors": len(ents), "header": args.header, "backend": args.backend,
-                       "auto_release": True, "global_batch": 1, "seq_len": 0,
-                       "parallelism": f"tp{world}" if world > 1 else "single",
-                       "data_plane": group.data_plane if world > 1 else None,
-                       "l2": f"inputs ({tensor_bytes / 1e9:.1f} GB) far exceed the 126 MB L2; no flush needed"},
-            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "seconds_to_ready": round(e2e_med / 1e3, 4),
-                    "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h, "page_cache": "warm",
-                    "io_modes": sorted(io_modes), "ring_setup_seconds_first_load": round(ring, 4),
-                    "page_cache_residency": resid, "host_memory_gb": host_mem,
-                    "first_load_seconds_in_process": round(first_ms / 1e3, 4) if first_ms else None,
-                    "phases_ms": phase_med},
+            "config": config,
+            "engine": {"backend": args.backend, "io_mode": args.io_mode or "backend default",
+                       "data_plane": list(groups)[0] if world > 1 else None},
+            "e2e": e2e,
             "e2e_cold": cold,
-            "e2e_views": views,
+            "planes": plane_out if world > 1 else None,
             "e2e_fresh_process": fresh,
             "library_baselines": libs,
             "roofline": roofline,
             "io_roofline": io,
+            "io_mode_cufile": ("measured: see e2e io_modes" if gds
+                               else "unavailable: no nvidia-fs (/proc/driver/nvidia-fs/stats absent); "
+                                    "the gds backend reads O_DIRECT through the pinned ring"),
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches_e2e,
-            "gpu_launches_value_leg": launches_value,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
