@@ -420,13 +420,41 @@ class DistGroup:
 
     def unpublish(self, imported: dict[str, int], own: set[str]) -> None:
         """Close peer mappings, then wait until every rank did, so owners may
-        free the memory."""
+        free the memory. A collective, bounded by ``timeout``: a rank that never
+        closes makes the others raise RendezvousTimeout instead of hanging."""
         from . import _native
 
         for f, p in imported.items():
             if f not in own:
                 _native.ipc_release(p)
-        self.barrier()
+        self.bounded_barrier("unpublish")
+
+    def bounded_barrier(self, tag: str, timeout: float | None = None) -> None:
+        """Barrier through the rendezvous store (a counter per call) that gives
+        up after ``timeout`` seconds (default: the group's) with
+        RendezvousTimeout — unlike a NCCL/gloo barrier, it cannot hang an
+        error path until the watchdog fires."""
+        if self.world_size == 1:
+            return
+        import time
+
+        from torch.distributed import distributed_c10d as c10d
+
+        store = c10d._get_default_store()
+        self._barrier_seq = getattr(self, "_barrier_seq", 0) + 1
+        members = "all" if self.pg is None else ",".join(map(str, c10d.get_process_group_ranks(self.pg)))
+        key = f"hl-barrier/{members}/{tag}/{self._barrier_seq}"
+        limit = self.timeout if timeout is None else timeout
+        deadline = time.monotonic() + limit
+        arrived = store.add(key, 1)
+        pause = 1e-4
+        while arrived < self.world_size:
+            if time.monotonic() > deadline:
+                raise RendezvousTimeout(f"rank {self.rank}: {arrived} of {self.world_size} ranks reached "
+                                        f"{tag!r} within {limit}s")
+            time.sleep(pause)
+            pause = min(pause * 2, 0.01)
+            arrived = store.add(key, 0)
 
     def barrier(self) -> None:
         if self.world_size > 1:

@@ -228,7 +228,10 @@ class DevicePool:
         per-key outputs of a checkpoint out of a few chunks (each sized by the
         announced remaining bytes, at most CARVE_CHUNK) turns a first load's
         ~1 s of allocator growth into a few calls. Accounting stays per buffer;
-        a chunk's memory returns when its last slice dies."""
+        a chunk's memory returns when its last slice dies — so a caller that
+        keeps one small output alive keeps its whole chunk (at most CARVE_CHUNK,
+        and never more than the handle's announced outputs) resident. With a
+        ``capacity_cap`` nothing is carved (``allocate``)."""
         if self._chunk is None or self._chunk_off + nbytes > self._chunk.numel():
             size = max(nbytes, min(CARVE_CHUNK, max(self._expect, nbytes)))
             self._chunk = torch.empty(size, dtype=torch.uint8, device=self.device)
@@ -254,8 +257,10 @@ class DevicePool:
                             f"device {self.device_id}: {size} bytes requested, "
                             f"{self.allocated_bytes} live of {self.capacity_cap} cap")
             try:
-                # +16: 16-byte vector loads of a tensor's last bytes stay inside the allocation
-                if carve:
+                # +16: 16-byte vector loads of a tensor's last bytes stay inside the allocation.
+                # Carving is off under a capacity cap: a chunk is device memory the cap's
+                # accounting (requested sizes) would not see.
+                if carve and self.capacity_cap is None:
                     try:
                         t = self._carve(max(size, 1) + 16)
                     except torch.OutOfMemoryError:

@@ -210,7 +210,9 @@ def read_header(path: str | os.PathLike, header_cap: int = DEFAULT_HEADER_CAP) -
     (ref format.py:166-189)."""
     path = Path(path)
     size = path.stat().st_size
-    with open(path, "rb", buffering=0) as f:
+    # buffered: read(n) loops until n bytes or EOF (a raw read is one syscall and may
+    # return short on FUSE / network mounts)
+    with open(path, "rb") as f:
         pre = f.read(8)
         if len(pre) < 8:
             raise TruncatedHeader(f"{path}: shorter than the 8-byte length prefix")

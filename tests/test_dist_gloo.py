@@ -77,6 +77,17 @@ def _worker(rank, world, port, q):
             out[f"scatter{dim}"] = (list(mine_shape), bytes(mine.numpy()))
             out["raw"] = raw
         out["bounds"] = [kernels.shard_bounds(7, world, r) for r in range(world)]
+        # the bounded (store-counter) barrier the peer-memory plane's close() uses:
+        # passes when everyone arrives, raises instead of hanging when a rank never does
+        g.bounded_barrier("both", timeout=30)
+        out["bounded"] = True
+        out["alone"] = True
+        if rank == 0:
+            try:
+                g.bounded_barrier("alone", timeout=0.5)
+                out["alone"] = "missed"
+            except RendezvousTimeout as e:
+                out["alone"] = "1 of 2" in str(e)
     finally:
         dist.destroy_process_group()
     q.put((rank, out))
@@ -100,6 +111,7 @@ def test_distgroup_two_ranks_gloo():
         assert res[r]["agree"] == "buffer"
         assert res[r]["mismatch"] is True
         assert res[r]["bcast"] == list(range(10))
+        assert res[r]["bounded"] is True and res[r]["alone"] is True
     raw = res[0]["raw"]
     full = np.frombuffer(raw, dtype=np.int16).reshape(7, 5)
     for dim in (0, 1):
