@@ -435,8 +435,9 @@ def run_cpu_reference(paths, keys, policy, steps: int, warmup: int, cold_steps: 
 # ----------------------------------------------------------------------------- io probes
 def io_probes(paths, device_index: int) -> dict:
     """Measured I/O roofline terms: pinned H2D (CUDA events) and cold storage
-    reads (tools/storage_probe.c: 64 O_DIRECT pread threads and one io_uring
-    at depth 64, file dropped from the page cache before each)."""
+    reads of the workload's files (tools/storage_probe.c: O_DIRECT pread
+    thread pools and io_uring rings over a sweep of depths and chunk sizes,
+    files dropped from the page cache before each); storage_gbs = the best."""
     import torch
 
     out = {}
@@ -455,10 +456,9 @@ def io_probes(paths, device_index: int) -> dict:
     out["h2d_gbs"] = round(4 * n / (e0.elapsed_time(e1) / 1e3) / 1e9, 3)
     del h, d
     probe = ROOT / "tools" / "build" / "storage_probe"
-    big = max(paths, key=os.path.getsize)
     if probe.exists():
-        try:
-            r = subprocess.run([str(probe), str(big), "quick"], capture_output=True, text=True, timeout=300)
+        try:  # every file of the workload as one job (what the engine reads), 8 configs
+            r = subprocess.run([str(probe), *map(str, paths)], capture_output=True, text=True, timeout=600)
             rows = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
             out["storage_probe"] = rows
             best = [x["GBps"] for x in rows if "GBps" in x]
@@ -467,7 +467,7 @@ def io_probes(paths, device_index: int) -> dict:
             out["storage_probe"] = f"{type(e).__name__}: {e}"[:200]
     else:
         out["storage_probe"] = "tools/build/storage_probe not built"
-    warm_cache([big])
+    warm_cache(paths)
     return out
 
 

@@ -93,8 +93,15 @@ typedef struct hl_config {
   uint32_t slots_per_worker; /* pinned ring depth per worker (0 = 3)                       */
   uint32_t io_mode;          /* enum hl_io_mode                                            */
   int32_t numa_node;         /* pin workers + ring to this node; -1 = the GPU's node       */
-  uint32_t reserved;
+  uint32_t flags;            /* HL_CFG_* bits                                              */
 } hl_config;
+
+/* HL_IO_AUTO: a chunk whose pages are all in the page cache is DMA'd straight
+ * from those pages (pinned in place with cudaHostRegister, like HL_IO_MMAP)
+ * instead of being copied into the pinned ring first: each delivered byte
+ * crosses host DRAM once instead of three times (page cache read + ring write
+ * + DMA read), which is what lets 8 GPUs of one host load warm files at once. */
+#define HL_CFG_AUTO_PIN_CACHE 1u
 
 /* One transfer block: file bytes [file_off, file_off+len) -> device address dev_dst.
  * Mirrors transfer.TransferBlock (ref transfer.py:135-142). */

@@ -36,8 +36,11 @@ class hl_config(C.Structure):
         ("slots_per_worker", C.c_uint32),
         ("io_mode", C.c_uint32),
         ("numa_node", C.c_int32),
-        ("reserved", C.c_uint32),
+        ("flags", C.c_uint32),
     ]
+
+
+HL_CFG_AUTO_PIN_CACHE = 1
 
 
 class hl_block(C.Structure):
@@ -200,16 +203,16 @@ class IoEngine:
     """One hl_ctx: worker threads' pinned ring + streams for one device."""
 
     def __init__(self, device: int, workers: int = 0, chunk_bytes: int = 0,
-                 slots_per_worker: int = 0, io_mode: str = "auto", numa_node: int = -1):
+                 slots_per_worker: int = 0, io_mode: str = "auto", numa_node: int = -1, flags: int = 0):
         lib = load()
-        cfg = hl_config(device, workers, chunk_bytes, slots_per_worker, IO_MODES[io_mode], numa_node, 0)
+        cfg = hl_config(device, workers, chunk_bytes, slots_per_worker, IO_MODES[io_mode], numa_node, flags)
         h = C.c_void_p()
         check(lib.hl_ctx_create(C.byref(cfg), C.byref(h)))
         self._h = h
         self._lib = lib
         eff = hl_config()
         check(lib.hl_ctx_config(h, C.byref(eff)))
-        self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_ if f != "reserved"}
+        self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_}
 
     def execute(self, paths: list[str], blocks: list[tuple[int, int, int, int, int]],
                 after_stream: int | None = None) -> dict:

@@ -422,12 +422,22 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
         s.reg = nullptr;
       }
     }
-    if (f.mode == HL_IO_MMAP) {
+    bool pin = f.mode == HL_IO_MMAP;
+    if (f.mode == HL_IO_AUTO && f.probe && (ctx->cfg.flags & HL_CFG_AUTO_PIN_CACHE)) {
+      // a fully resident chunk is DMA'd from the page cache in place (one DRAM pass)
+      const uint64_t p0 = c.off / kAlign, p1 = (c.off + c.len + kAlign - 1) / kAlign;
+      if (vec.size() < p1 - p0) vec.resize(p1 - p0);
+      pin = mincore(f.probe + p0 * kAlign, (p1 - p0) * kAlign, vec.data()) == 0;
+      for (uint64_t q = 0; pin && q < p1 - p0; ++q) pin = vec[q] & 1;
+    }
+    if (pin) {
       // pin the page-cache pages of this chunk in place and DMA them: no CPU copy
-      uint8_t* p = f.map + c.off;
+      uint8_t* p = (f.map ? f.map : f.probe) + c.off;
       uint8_t* a = (uint8_t*)round_down((uint64_t)(uintptr_t)p, kAlign);
       const uint64_t alen = round_up((uint64_t)(p - a) + c.len, kAlign);
+      const double tp = now_s();
       cudaError_t e = cudaHostRegister(a, alen, cudaHostRegisterPortable | cudaHostRegisterReadOnly);
+      run->read_ns += (uint64_t)((now_s() - tp) * 1e9);
       if (e == cudaSuccess) {
         e = cudaMemcpyAsync((void*)c.dst, p, c.len, cudaMemcpyHostToDevice, ring.stream);
         if (e == cudaSuccess) e = cudaEventRecord(s.ev, ring.stream);

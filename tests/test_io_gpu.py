@@ -12,7 +12,7 @@ from paper_2505_23072_b200.errors import IoError  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-MODES = ["buffered", "direct", "auto", "cufile", "mmap"]
+MODES = ["buffered", "direct", "auto", "cufile", "mmap", "auto-pin"]
 
 
 @pytest.fixture(scope="module")
@@ -27,7 +27,11 @@ def blob(tmp_path_factory):
 @pytest.mark.parametrize("mode", MODES)
 def test_ranges_land_exactly(blob, mode):
     path, data = blob
-    eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode=mode)
+    if mode == "auto-pin":  # resident chunks DMA'd from the page cache in place (HL_CFG_AUTO_PIN_CACHE)
+        eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode="auto", flags=_native.HL_CFG_AUTO_PIN_CACHE)
+        path.read_bytes()  # resident
+    else:
+        eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode=mode)
     rng = np.random.default_rng(3)
     ranges = [(0, data.size), (1, 4095), (4096, 8192), (13281, (5 << 20) + 7), (data.size - 9, 9)]
     for _ in range(6):
@@ -47,6 +51,8 @@ def test_ranges_land_exactly(blob, mode):
         assert np.array_equal(got[cur:cur + n], data[off:off + n]), (mode, off, n)
         cur += n
     assert st["io_modes"], st
+    if mode == "auto-pin":
+        assert "mmap" in st["io_modes"] and st["mmap_bytes"] > total // 2, st
     eng.close()
 
 

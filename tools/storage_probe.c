@@ -2,8 +2,8 @@
 // O_DIRECT reads, (a) T threads of synchronous pread, (b) one io_uring ring at
 // queue depth Q (raw syscalls, no liburing). Prints one JSON line per config.
 //   gcc -O2 -pthread -o /tmp/storage_probe tools/storage_probe.c
-//   /tmp/storage_probe FILE [quick]  (drops the file from the page cache before each run;
-//                                     quick: the two configs that measured best, for bench.py)
+//   /tmp/storage_probe FILE... [quick]  (reads all FILEs as one job, dropped from the page
+//                                        cache before each run; quick: two configs only)
 #define _GNU_SOURCE
 #include <fcntl.h>
 #include <linux/io_uring.h>
@@ -19,9 +19,20 @@
 #include <time.h>
 #include <unistd.h>
 
-static const char* g_path;
-static uint64_t g_size, g_chunk;
+#define MAXF 64
+static const char* g_paths[MAXF];
+static uint64_t g_sizes[MAXF], g_starts[MAXF];
+static int g_nfiles;
+static uint64_t g_size, g_chunk;  // g_size: sum of the files' 4 KiB-rounded-down sizes
 static atomic_uint_fast64_t g_cursor;
+
+// global offset -> (file, offset); a chunk never crosses a file end (callers clip)
+static int locate(uint64_t off, uint64_t* local) {
+  int f = 0;
+  while (f + 1 < g_nfiles && off >= g_starts[f + 1]) ++f;
+  *local = off - g_starts[f];
+  return f;
+}
 
 static double now(void) {
   struct timespec t;
@@ -30,26 +41,30 @@ static double now(void) {
 }
 
 static void drop(void) {
-  int fd = open(g_path, O_RDONLY);
-  fdatasync(fd);
-  posix_fadvise(fd, 0, 0, POSIX_FADV_DONTNEED);
-  close(fd);
+  for (int i = 0; i < g_nfiles; ++i) {
+    int fd = open(g_paths[i], O_RDONLY);
+    fdatasync(fd);
+    posix_fadvise(fd, 0, 0, POSIX_FADV_DONTNEED);
+    close(fd);
+  }
 }
 
 static void* worker(void* arg) {
   (void)arg;
-  int fd = open(g_path, O_RDONLY | O_DIRECT);
+  int fds[MAXF];
+  for (int i = 0; i < g_nfiles; ++i) fds[i] = open(g_paths[i], O_RDONLY | O_DIRECT);
   void* buf;
   if (posix_memalign(&buf, 4096, g_chunk)) return NULL;
   for (;;) {
     uint64_t off = atomic_fetch_add(&g_cursor, g_chunk);
     if (off >= g_size) break;
-    uint64_t n = g_size - off < g_chunk ? g_size - off : g_chunk;
-    n = (n + 4095) & ~4095ull;
-    if (pread(fd, buf, n, off) < 0) break;
+    uint64_t local;
+    const int f = locate(off, &local);
+    uint64_t n = g_sizes[f] - local < g_chunk ? g_sizes[f] - local : g_chunk;
+    if (pread(fds[f], buf, n, local) < 0) break;
   }
   free(buf);
-  close(fd);
+  for (int i = 0; i < g_nfiles; ++i) close(fds[i]);
   return NULL;
 }
 
@@ -97,7 +112,8 @@ static void uring(unsigned qd, uint64_t chunk) {
   unsigned* cq_tail = (unsigned*)(cq + p.cq_off.tail);
   unsigned* cq_mask = (unsigned*)(cq + p.cq_off.ring_mask);
   struct io_uring_cqe* cqes = (struct io_uring_cqe*)(cq + p.cq_off.cqes);
-  int fd = open(g_path, O_RDONLY | O_DIRECT);
+  int fds[MAXF];
+  for (int i = 0; i < g_nfiles; ++i) fds[i] = open(g_paths[i], O_RDONLY | O_DIRECT);
   uint8_t* bufs;
   if (posix_memalign((void**)&bufs, 4096, (size_t)qd * chunk)) return;
   uint64_t next = 0, done = 0;
@@ -114,12 +130,14 @@ static void uring(unsigned qd, uint64_t chunk) {
       unsigned idx = tail & *sq_mask;
       struct io_uring_sqe* e = &sqes[idx];
       memset(e, 0, sizeof *e);
-      uint64_t n = g_size - next < chunk ? g_size - next : chunk;
+      uint64_t local;
+      const int f = locate(next, &local);
+      uint64_t n = g_sizes[f] - local < chunk ? g_sizes[f] - local : chunk;
       e->opcode = IORING_OP_READ;
-      e->fd = fd;
+      e->fd = fds[f];
       e->addr = (uint64_t)(uintptr_t)(bufs + (size_t)slot * chunk);
-      e->len = (uint32_t)((n + 4095) & ~4095ull);
-      e->off = next;
+      e->len = (uint32_t)n;
+      e->off = local;
       e->user_data = ((uint64_t)slot << 40) | n;
       sq_array[idx] = idx;
       __atomic_store_n(sq_tail, tail + 1, __ATOMIC_RELEASE);
@@ -144,18 +162,27 @@ static void uring(unsigned qd, uint64_t chunk) {
   printf("{\"probe\": \"io_uring\", \"qd\": %u, \"chunk_mb\": %.2f, \"GBps\": %.3f}\n", qd, chunk / 1048576.0,
          g_size / dt / 1e9);
   fflush(stdout);
-  close(fd);
+  for (int i = 0; i < g_nfiles; ++i) close(fds[i]);
   close(rfd);
   free(bufs);
 }
 
 int main(int argc, char** argv) {
-  if (argc < 2) return 2;
-  g_path = argv[1];
-  struct stat st;
-  if (stat(g_path, &st)) return 2;
-  g_size = (uint64_t)st.st_size & ~4095ull;
-  if (argc > 2 && strcmp(argv[2], "quick") == 0) {
+  int quick = 0;
+  for (int i = 1; i < argc && g_nfiles < MAXF; ++i) {
+    if (strcmp(argv[i], "quick") == 0) {
+      quick = 1;
+      continue;
+    }
+    struct stat st;
+    if (stat(argv[i], &st)) return 2;
+    g_paths[g_nfiles] = argv[i];
+    g_sizes[g_nfiles] = (uint64_t)st.st_size & ~4095ull;
+    g_starts[g_nfiles] = g_size;
+    g_size += g_sizes[g_nfiles++];
+  }
+  if (!g_nfiles) return 2;
+  if (quick) {
     threads(64, 4 << 20);
     uring(64, 1 << 20);
     return 0;
