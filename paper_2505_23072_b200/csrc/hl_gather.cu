@@ -37,8 +37,12 @@
 //     stages, consumer warps shift/convert into smem output stages, TMA bulk
 //     stores). Both stride 8-16 KiB units per CTA. Multi-row (column shard)
 //     descriptors stay on the warp kernels above.
+#include <cuda.h>  // CUtensorMap (encoded through cudaGetDriverEntryPoint: no -lcuda)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include <atomic>
 #include <mutex>
@@ -846,6 +850,189 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
   }
 }
 
+// ---------------------------------------------------------------- TMA tensor tiles (column shards)
+// Multi-row descriptors (a rank's column shard: `rows` row segments of a few
+// KiB at a fixed source pitch, ref collective.py:318-330 _clone_slice along
+// dim >= 1) move as 2-D boxes of a tensor map: the source is described as a
+// rows x cols matrix at the tensor's pitch, the destination as the dense
+// rows x seg matrix, and a box is BY rows x BX columns (<= 16 KiB). One
+// elected thread per CTA streams boxes HBM -> shared memory with
+// cp.async.bulk.tensor.2d (UTMALDG: the TMA unit walks the strided rows, no
+// per-row address arithmetic in any warp) and writes them back with
+// cp.async.bulk.tensor.2d stores (UTMASTG, clipped to the shard's edges by the
+// destination map). Casts add consumer warps that convert each staged box in
+// shared memory into an output box first (staged_kernel's scheme). Raw copies
+// use the widest element (8/4/2/1 B) the shard's offsets allow, so a box row
+// is up to 2 KiB of contiguous source bytes.
+constexpr uint32_t kTileBox = 16u << 10;  // bytes of one box (input and output)
+#ifndef HL_TILE_STAGES
+#define HL_TILE_STAGES 6
+#endif
+#ifndef HL_TILE_CAST_STAGES
+#define HL_TILE_CAST_STAGES 3
+#endif
+constexpr int kTileStages = HL_TILE_STAGES;          // raw copies: 1 thread, 1 CTA per SM
+constexpr int kTileCastStages = HL_TILE_CAST_STAGES;  // casts: in + out stage each, 2 CTAs per SM
+constexpr int kTileConsumerWarps = 8;
+constexpr int kTileCastThreads = 32 * (1 + kTileConsumerWarps);
+constexpr int kMaxTiles = 96;  // 64 + 96 * 320 = 30784 B of kernel parameters
+
+struct alignas(64) TileDesc {
+  CUtensorMap src;      // {cols, rows} at the source pitch; element = the copy unit or the src dtype
+  CUtensorMap dst;      // {seg cols, rows} dense
+  uint64_t unit_begin;  // first unit (box) of this descriptor in the launch
+  uint32_t nbx;         // boxes across the segment
+  int32_t c0;           // first source column of the segment (tensor-map elements)
+  uint32_t bx, by;      // box dims (elements, rows)
+  uint32_t in_bytes;    // bytes of one source box (mbarrier transaction count)
+};
+static_assert(sizeof(TileDesc) == 320, "TileDesc layout");
+
+struct TileParams {
+  uint32_t n;
+  uint32_t pad;
+  uint64_t total_units;
+  TileDesc d[kMaxTiles];
+};
+
+struct TileUnit {
+  const TileDesc* d;
+  int32_t sx, sy, dx;  // source box origin (col, row), destination col (row = sy)
+};
+
+__device__ __forceinline__ TileUnit tile_unit(const TileParams& p, uint64_t u, uint32_t& di) {
+  while (di + 1 < p.n && p.d[di + 1].unit_begin <= u) ++di;
+  const TileDesc& d = p.d[di];
+  const uint64_t lu = u - d.unit_begin;
+  const uint32_t by = (uint32_t)(lu / d.nbx), bx = (uint32_t)(lu % d.nbx);
+  TileUnit t;
+  t.d = &d;
+  t.dx = (int32_t)(bx * d.bx);
+  t.sx = d.c0 + t.dx;
+  t.sy = (int32_t)(by * d.by);
+  return t;
+}
+
+__device__ __forceinline__ void tile_load(const TileUnit& t, uint32_t smem, uint32_t bar, uint64_t policy) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(t.d->in_bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      :: "r"(smem), "l"(&t.d->src), "r"(t.sx), "r"(t.sy), "r"(bar), "l"(policy) : "memory");
+}
+
+__device__ __forceinline__ void tile_store(const TileUnit& t, uint32_t smem, uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;"
+               :: "l"(&t.d->dst), "r"(t.dx), "r"(t.sy), "r"(smem), "l"(policy) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Raw column shards: load box -> store the same shared-memory box.
+__global__ void __launch_bounds__(32) tile_copy_kernel(const __grid_constant__ TileParams p) {
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bar[kTileStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kTileStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
+  uint32_t ldi = 0, sdi = 0;
+  constexpr uint64_t ahead = kTileStages - 1;  // one store may still be reading its stage
+  for (uint64_t k = 0; k < mine && k < ahead; ++k) {
+    const int s = (int)(k % kTileStages);
+    tile_load(tile_unit(p, first + k * step, ldi), smem_u32(stage + (size_t)s * kTileBox), smem_u32(&bar[s]), policy);
+  }
+  for (uint64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % kTileStages);
+    const TileUnit t = tile_unit(p, first + k * step, sdi);
+    mbar_wait(smem_u32(&bar[s]), (uint32_t)((k / kTileStages) & 1));
+    tile_store(t, smem_u32(stage + (size_t)s * kTileBox), policy);
+    if (k + ahead < mine) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // store k-1 has read its stage
+      const uint64_t j = k + ahead;
+      const int sj = (int)(j % kTileStages);
+      tile_load(tile_unit(p, first + j * step, ldi), smem_u32(stage + (size_t)sj * kTileBox), smem_u32(&bar[sj]),
+                policy);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Cast column shards: producer lane loads boxes, consumer warps convert box s
+// (flat element order: the in and out boxes have the same rows x cols) into
+// output stage s, the producer stores it.
+template <int K>
+__global__ void __launch_bounds__(kTileCastThreads) tile_cast_kernel(const __grid_constant__ TileParams p) {
+  constexpr uint32_t NB = KindTraits<K>::NB;  // source bytes per 16-byte output vector
+  extern __shared__ __align__(128) uint8_t stage[];
+  uint8_t* const outs = stage + (size_t)kTileCastStages * kTileBox;
+  __shared__ __align__(8) uint64_t full[kTileCastStages], empty[kTileCastStages];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTileCastStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(kTileConsumerWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
+  if (warp == 0) {
+    if (lane != 0) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    uint32_t ldi = 0, sdi = 0;
+    for (uint64_t k = 0; k < mine && k < (uint64_t)kTileCastStages; ++k) {
+      const int s = (int)(k % kTileCastStages);
+      tile_load(tile_unit(p, first + k * step, ldi), smem_u32(stage + (size_t)s * kTileBox), smem_u32(&full[s]),
+                policy);
+    }
+    for (uint64_t k = 0; k < mine; ++k) {
+      const int s = (int)(k % kTileCastStages);
+      const TileUnit t = tile_unit(p, first + k * step, sdi);
+      mbar_wait(smem_u32(&empty[s]), (uint32_t)((k / kTileCastStages) & 1));  // box k converted
+      tile_store(t, smem_u32(outs + (size_t)s * kTileBox), policy);
+      if (k + kTileCastStages < mine) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // output stage s read out
+        const uint64_t j = k + kTileCastStages;
+        tile_load(tile_unit(p, first + j * step, ldi), smem_u32(stage + (size_t)s * kTileBox), smem_u32(&full[s]),
+                  policy);
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    return;
+  }
+  const uint32_t ct = threadIdx.x - 32;
+  constexpr uint32_t CT = 32 * kTileConsumerWarps;
+  uint32_t di = 0;
+  for (uint64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % kTileCastStages);
+    const TileUnit t = tile_unit(p, first + k * step, di);
+    const uint32_t nv = t.d->in_bytes / NB;  // output vectors of the box
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kTileCastStages) & 1));
+    const uint8_t* in = stage + (size_t)s * kTileBox;
+    uint8_t* out = outs + (size_t)s * kTileBox;
+    for (uint32_t v = ct; v < nv; v += CT) {
+      Span<NB> sp;
+      if constexpr (NB == 8) {
+        const uint64_t x = *reinterpret_cast<const uint64_t*>(in + (size_t)v * 8);
+        sp.v[0] = make_uint4((uint32_t)x, (uint32_t)(x >> 32), 0, 0);
+      } else {
+#pragma unroll
+        for (int j = 0; j < (int)(NB / 16); ++j) sp.v[j] = lds16(in + (size_t)v * NB + 16 * j);
+      }
+      *reinterpret_cast<uint4*>(out + (size_t)v * 16) = convert_vec<K>(sp);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- host side
 static const uint32_t kSize[13] = {1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8};
 
@@ -1014,6 +1201,124 @@ static int make_kdesc(const hl_desc& h, uint32_t i, KDesc out[2], uint64_t units
   return HL_OK;
 }
 
+// ---- TMA tensor tiles (host): tensor maps for column-shard descriptors
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static EncodeTiled encode_tiled() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+static bool tiles_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HL_GATHER_TILES");
+    return !(e && e[0] == '0');
+  }();
+  return on && encode_tiled() != nullptr;
+}
+
+static CUtensorMapDataType tmap_type(uint32_t bytes) {
+  switch (bytes) {
+    case 1: return CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    case 2: return CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    case 4: return CU_TENSOR_MAP_DATA_TYPE_UINT32;
+    default: return CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  }
+}
+
+// A column shard the tile kernels take: several rows, a source pitch larger
+// than the row, 16-byte aligned destination rows of at least 64 bytes.
+// Fills `t` (all but unit_begin) and its unit (box) count; false = not a tile.
+static bool make_tile(const hl_desc& h, int kind, TileDesc& t, uint64_t& units) {
+  const uint32_t ss = kSize[h.src_dtype], ds = kSize[h.dst_dtype];
+  if (h.rows < 2 || h.row_elems == 0) return false;
+  const uint64_t in_row = h.row_elems * ss, out_row = h.row_elems * ds;
+  if (h.src_pitch == in_row) return false;  // contiguous rows: bulk / staged kernels
+  if (h.dst % 16 || out_row % 16 || out_row < 64 || h.src_pitch % 16 || h.src % ss) return false;
+  if (h.src_pitch >= (1ull << 40) || h.rows >= (1ull << 31)) return false;
+  const uint64_t base = h.src & ~15ull;
+  const uint32_t lead = (uint32_t)(h.src - base);
+  uint32_t ui = ss, uo = ds;  // tensor-map element bytes
+  if (kind == K_COPY1) {      // raw bytes: the widest unit the offsets allow
+    uint32_t u = 8;
+    while (u > 1 && (lead % u || in_row % u)) u >>= 1;
+    ui = uo = u;
+  }
+  const uint64_t cols = in_row / ui;  // = out_row / uo
+  const uint32_t wide = std::max(ui, uo), g = 16 / std::min(ui, uo);
+  const uint64_t bx_max = std::min<uint64_t>(256, 2048 / wide);
+  const uint32_t bx = (uint32_t)std::min<uint64_t>(bx_max, (cols + g - 1) / g * g);
+  const uint32_t by = (uint32_t)std::min<uint64_t>({256, kTileBox / ((uint64_t)bx * wide), h.rows});
+  t.c0 = (int32_t)(lead / ui);
+  t.bx = bx;
+  t.by = by;
+  t.nbx = (uint32_t)((cols + bx - 1) / bx);
+  t.in_bytes = bx * by * ui;
+  units = (uint64_t)t.nbx * ((h.rows + by - 1) / by);
+  const cuuint32_t box[2] = {bx, by}, estr[2] = {1, 1};
+  const cuuint64_t sdim[2] = {t.c0 + cols, h.rows}, sstr[1] = {h.src_pitch};
+  const cuuint64_t ddim[2] = {cols, h.rows}, dstr[1] = {out_row};
+  EncodeTiled enc = encode_tiled();
+  if (enc(&t.src, tmap_type(ui), 2, reinterpret_cast<void*>(base), sdim, sstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (enc(&t.dst, tmap_type(uo), 2, reinterpret_cast<void*>(h.dst), ddim, dstr, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  return true;
+}
+
+static auto tile_kernel_of(int kind) -> void (*)(TileParams) {
+  switch (kind) {
+    case K_COPY1: return tile_copy_kernel;
+    case K_BF16_F16: return tile_cast_kernel<K_BF16_F16>;
+    case K_F32_F16: return tile_cast_kernel<K_F32_F16>;
+    case K_F16_F32: return tile_cast_kernel<K_F16_F32>;
+    default: return tile_cast_kernel<K_BF16_F32>;
+  }
+}
+static size_t tile_smem(int kind) {
+  return kind == K_COPY1 ? (size_t)kTileStages * kTileBox : (size_t)2 * kTileCastStages * kTileBox;
+}
+
+static int launch_tiles(int kind, TileParams& p, cudaStream_t stream) {
+  if (p.total_units == 0) return HL_OK;
+  static std::mutex mu;
+  static bool attr_set[64][5] = {};
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!attr_set[dev & 63][kind]) {
+      cudaFuncSetAttribute(tile_kernel_of(kind), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem(kind));
+      attr_set[dev & 63][kind] = true;
+    }
+  }
+  const uint64_t cap = (uint64_t)sms * (kind == K_COPY1 ? 1 : 2);
+  const unsigned grid = (unsigned)std::min<uint64_t>(p.total_units, cap);
+  tile_kernel_of(kind)<<<grid, kind == K_COPY1 ? 32 : kTileCastThreads, tile_smem(kind), stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HL_ECUDA, "tile launch failed: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  p.n = 0;
+  p.total_units = 0;
+  return HL_OK;
+}
+
 static int launch(int kind, int which, Params& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
   const bool bulk = is_bulk(kind, which), staged = is_staged(which);
@@ -1068,6 +1373,12 @@ extern "C" int hl_gather_prepare(int device) {
       grid_cap(kind, which);  // the Params variant: occupancy / shared-memory attributes
     }
   }
+  for (int kind = 0; kind < 5; ++kind) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, tile_kernel_of(kind));
+    cudaFuncSetAttribute(tile_kernel_of(kind), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem(kind));
+  }
+  encode_tiled();
   cudaGetLastError();
   cudaSetDevice(prev);
   return HL_OK;
@@ -1090,7 +1401,24 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
   uint64_t ku[2];
   int cnt = 0;
   uint32_t present = 0;  // bitmask of non-empty buckets
+  static thread_local std::vector<TileDesc> tiles[5];  // column shards per conversion kind
+  static thread_local std::vector<uint64_t> tile_units[5];
+  for (int k = 0; k < 5; ++k) {
+    tiles[k].clear();
+    tile_units[k].clear();
+  }
+  const bool use_tiles = tma && tiles_enabled();
   for (uint32_t i = 0; i < n; ++i) {
+    if (use_tiles) {
+      const int kind = conversion_kind(descs[i].src_dtype, descs[i].dst_dtype);
+      TileDesc t;
+      uint64_t tu = 0;
+      if (kind >= 0 && descs[i].src && descs[i].dst && make_tile(descs[i], kind, t, tu)) {
+        tiles[kind].push_back(t);
+        tile_units[kind].push_back(tu);
+        continue;
+      }
+    }
     int rc = make_kdesc(descs[i], i, kd, ku, &cnt, tma);
     if (rc) return rc;
     for (int j = 0; j < cnt; ++j) {
@@ -1120,6 +1448,24 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
       }
     }
     int rc = launch(kind, which, *p, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  static thread_local TileParams* tp = nullptr;  // ~30 KB
+  for (int kind = 0; kind < 5; ++kind) {
+    if (tiles[kind].empty()) continue;
+    if (!tp) tp = new TileParams();
+    tp->n = 0;
+    tp->total_units = 0;
+    for (size_t i = 0; i < tiles[kind].size(); ++i) {
+      tiles[kind][i].unit_begin = tp->total_units;
+      tp->d[tp->n++] = tiles[kind][i];
+      tp->total_units += tile_units[kind][i];
+      if (tp->n == (uint32_t)kMaxTiles) {
+        int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
+        if (rc) return rc;
+      }
+    }
+    int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return HL_OK;

@@ -249,3 +249,71 @@ def test_no_tma_flag_gives_identical_bytes():
     assert_same(outs[1], outs[0])
     _, exp = run_both(src, cd, descs)
     assert_same(outs[0], exp)
+
+
+TILE_KINDS = [(10, 10), (1, 1), (11, 11), (7, 7), (10, 9), (11, 9), (9, 11), (10, 11)]
+
+
+@pytest.mark.parametrize("sdt,ddt", TILE_KINDS)
+@pytest.mark.parametrize("seed", range(5))
+def test_column_shard_tiles(sdt, ddt, seed):
+    """Column shards (rows > 1, pitch > row): the 2-D tensor-map TMA kernels
+    (tile_copy_kernel / tile_cast_kernel) — box edges inside and at the end of
+    rows, ragged last boxes, >256 rows, every rank of W = 2/3/8 (source
+    offsets at every element position), plus the narrow-row / odd-width cases
+    that stay on the warp kernels; all against the oracle, with sentinels."""
+    rng = np.random.default_rng(1000 * seed + 10 * sdt + ddt)
+    ss, ds = SIZES[sdt], SIZES[ddt]
+    world = int(rng.choice([2, 3, 8]))
+    rows = int(rng.choice([2, 33, 257, 600]))
+    cols = int(rng.choice([64, 96, 1000, 1024, 4096, 2304])) * max(1, 8 // ss)
+    lead = int(rng.choice([0, ss, 16]))
+    src = rng.integers(0, 256, size=lead + rows * cols * ss + 64, dtype=np.uint8)
+    descs, cd = [], 0
+    for r in range(world):
+        lo, hi = kernels.shard_bounds(cols, world, r)
+        descs.append((lead + lo * ss, cd, rows, hi - lo, cols * ss, sdt, ddt))
+        cd = (cd + rows * (hi - lo) * ds + 15) & ~15
+    got, exp = run_both(src, cd, descs)
+    assert_same(got, exp)
+
+
+@pytest.mark.parametrize("shape,dt,cast", [((4096, 8192), 10, None), ((4096, 8192), 10, 9),
+                                           ((2048, 3072), 11, 9), ((1024, 5120), 10, 11)])
+def test_tp8_column_shards_large(shape, dt, cast):
+    """70B-sized column shards (TP=8 along dim 1): the owner-pack batch of the
+    NCCL plane and the C4/C5 workload shape, bit-exact."""
+    rng = np.random.default_rng(shape[1] + dt)
+    rows, cols = shape
+    ss = SIZES[dt]
+    ddt = cast or dt
+    src = rng.integers(0, 256, size=rows * cols * ss + 64, dtype=np.uint8)
+    descs, cd = [], 0
+    for r in range(8):
+        lo, hi = kernels.shard_bounds(cols, 8, r)
+        descs.append((lo * ss, cd, rows, hi - lo, cols * ss, dt, ddt))
+        cd = (cd + rows * (hi - lo) * SIZES[ddt] + 15) & ~15
+    got, exp = run_both(src, cd, descs)
+    assert_same(got, exp)
+
+
+def test_many_column_shards_span_tile_launches():
+    """More column-shard descriptors than one tile launch carries (96): the
+    launch split and the per-descriptor unit walk."""
+    rng = np.random.default_rng(77)
+    src = rng.integers(0, 256, size=16 << 20, dtype=np.uint8)
+    descs, cs, cd = [], 0, 0
+    for i in range(250):
+        rows = int(rng.integers(2, 40))
+        cols = 8 * int(rng.integers(8, 200))
+        seg = 8 * int(rng.integers(4, cols // 8 + 1))
+        lo = 8 * int(rng.integers(0, (cols - seg) // 8 + 1))
+        sdt, ddt = [(10, 10), (10, 9), (1, 1)][i % 3]
+        ss = SIZES[sdt]
+        if cs + rows * cols * ss + 64 > src.size:
+            break
+        descs.append((cs + lo * ss, cd, rows, seg, cols * ss, sdt, ddt))
+        cs = (cs + rows * cols * ss + 15) & ~15
+        cd = (cd + rows * seg * SIZES[ddt] + 15) & ~15
+    got, exp = run_both(src, cd, descs)
+    assert_same(got, exp)
