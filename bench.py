@@ -602,9 +602,9 @@ def main():
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # at N ranks every rank must own file bytes: re-split only when the HF split has fewer than N files
-    hf_files = len(synth_split(args.arch, args.layers))
-    n_files = args.files if args.files else (None if world <= hf_files else world)
+    # N > 1: the checkpoint re-split into N roughly equal files, round-robin one per rank (the HF
+    # split's 9.9 + 3.5 GB would leave rank 0 with 3x the bytes of rank 1 at N=2)
+    n_files = args.files if args.files else (None if world == 1 else world)
     paths = ensure_data(args.arch, args.data_dir, args.header, rank, world, dist, n_files, args.layers)
     from paper_2505_23072_b200 import kernels, synth
     from paper_2505_23072_b200.format import DType

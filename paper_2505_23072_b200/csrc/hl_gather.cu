@@ -1246,14 +1246,19 @@ static bool make_tile(const hl_desc& h, int kind, TileDesc& t, uint64_t& units) 
   if (h.rows < 2 || h.row_elems == 0) return false;
   const uint64_t in_row = h.row_elems * ss, out_row = h.row_elems * ds;
   if (h.src_pitch == in_row) return false;  // contiguous rows: bulk / staged kernels
-  if (h.dst % 16 || out_row % 16 || out_row < 64 || h.src_pitch % 16 || h.src % ss) return false;
+  // A box whose first byte is not 16-byte aligned faults the TMA unit (illegal
+  // instruction; tools/tile_probe.cu, profiles/r02_tile_probe.jsonl), so the
+  // segment must start 16-byte aligned: every TP=2/4/8 shard of an LLM weight
+  // does; others (TP=3 of 4096 columns, realigned odd landings) stay on the
+  // LDG/STG row kernel.
+  if (h.dst % 16 || h.src % 16 || out_row % 16 || out_row < 64 || h.src_pitch % 16) return false;
   if (h.src_pitch >= (1ull << 40) || h.rows >= (1ull << 31)) return false;
-  const uint64_t base = h.src & ~15ull;
-  const uint32_t lead = (uint32_t)(h.src - base);
+  const uint64_t base = h.src;
+  const uint32_t lead = 0;
   uint32_t ui = ss, uo = ds;  // tensor-map element bytes
-  if (kind == K_COPY1) {      // raw bytes: the widest unit the offsets allow
+  if (kind == K_COPY1) {      // raw bytes: the widest unit the row allows
     uint32_t u = 8;
-    while (u > 1 && (lead % u || in_row % u)) u >>= 1;
+    while (u > 1 && in_row % u) u >>= 1;
     ui = uo = u;
   }
   const uint64_t cols = in_row / ui;  // = out_row / uo

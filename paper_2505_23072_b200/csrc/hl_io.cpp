@@ -451,6 +451,12 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
         continue;
       }
       cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
+      if (getenv("HL_IO_DEBUG"))
+        fprintf(stderr, "hl_io: cudaHostRegister(%p, %llu) refused: %s\n", (void*)a, (unsigned long long)alen,
+                cudaGetErrorString(e));
+    } else if (getenv("HL_IO_DEBUG") && f.mode == HL_IO_AUTO) {
+      fprintf(stderr, "hl_io: chunk at %llu not pinned (flags %u, probe %p)\n", (unsigned long long)c.off,
+              ctx->cfg.flags, (void*)f.probe);
     }
     if (!s.host) {
       int rc = ensure_slot(ctx, w, (uint32_t)(&s - ring.slots.data()), s);

@@ -143,11 +143,14 @@ class DeviceBuffer:
         self.refcount = 0
         self.released = False
         self._live_views: weakref.WeakSet = weakref.WeakSet()
+        self._pending = None  # a deferred retrieval batch that still has to write this buffer
 
     @property
     def tensor(self) -> torch.Tensor:
         if self.released:
             raise DoubleRelease(f"buffer on device {self.device_id} was already released")
+        if self._pending is not None:
+            self._pending.flush()
         return self._tensor
 
     # reference spelling: the raw byte array behind the buffer

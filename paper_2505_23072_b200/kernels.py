@@ -45,8 +45,8 @@ def shard_desc(src_ptr: int, shape: tuple[int, ...], dim: int, lo: int, hi: int,
             src.code, dst.code)
 
 
-def stream_ptr(device: torch.device) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
+def current_stream_ptr(device: torch.device) -> int:
+    return _raw_stream(device.index)
 
 
 # Optional launch timing (bench.py): when a list, every run() appends
@@ -68,21 +68,23 @@ except AttributeError:  # pragma: no cover
         return torch.cuda.current_stream(index).cuda_stream
 
 
-def run(descs: list[Desc], device: torch.device, peer: bool = False) -> None:
-    """Enqueue the batch on ``device``'s current stream. hl_gather launches on
-    the CURRENT device (grid sizing and the launch itself), so switch to the
-    stream's device when the caller's differs. ``peer``: some sources are
-    another GPU's memory (peer pulls) — keep them on the LDG/STG kernels."""
+def run(descs: list[Desc], device: torch.device, peer: bool = False, stream_ptr: int | None = None) -> None:
+    """Enqueue the batch on ``device``'s current stream (or on ``stream_ptr``,
+    a cudaStream_t of that device). hl_gather launches on the CURRENT device
+    (grid sizing and the launch itself), so switch to the stream's device when
+    the caller's differs. ``peer``: some sources are another GPU's memory (peer
+    pulls) — keep them on the LDG/STG kernels."""
     if not descs:
         return
     if torch.cuda.current_device() != device.index:
         with torch.cuda.device(device):
-            return run(descs, device, peer)
+            return run(descs, device, peer, stream_ptr)
     flags = _native.GATHER_NO_TMA if peer else 0
     if TIMING is None:
-        _native.gather(descs, _raw_stream(device.index), flags)
+        _native.gather(descs, _raw_stream(device.index) if stream_ptr is None else stream_ptr, flags)
         return
-    stream = torch.cuda.current_stream(device)
+    stream = torch.cuda.current_stream(device) if stream_ptr is None else \
+        torch.cuda.ExternalStream(stream_ptr, device=device)
     table, n = _native.pack(descs)  # host-side table build stays outside the timed launch
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)

@@ -15,7 +15,7 @@ caller already holds stays valid (torch reference counting keeps the storage).
 from __future__ import annotations
 
 import struct
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Sequence
 
 import numpy as np
@@ -65,14 +65,40 @@ class Element:
     bits: int
 
 
-@dataclass(frozen=True, eq=False)
 class TensorView:
-    buffer: DeviceBuffer
-    base_offset: int
-    dtype: DType
-    shape: tuple[int, ...]
-    strides: tuple[int, ...] = field(default=())
-    torch: torch.Tensor | None = field(default=None, repr=False)
+    """``(buffer, base_offset, dtype, shape)`` over HBM (ref tensorview.py:55-128),
+    plus ``.torch``: the typed CUDA tensor aliasing those bytes. The torch view
+    and the byte strides are built on first use (a retrieval hands out hundreds
+    of views; most callers touch ``.torch`` once, some never); the view keeps
+    the storage it aliases, so ``.torch`` stays valid after the loader released
+    the buffer, exactly like a tensor taken before the release."""
+
+    __slots__ = ("buffer", "base_offset", "dtype", "shape", "_strides", "_torch", "_storage", "__weakref__")
+
+    def __init__(self, buffer: DeviceBuffer, base_offset: int, dtype: DType, shape: tuple[int, ...],
+                 strides: tuple[int, ...] | None = None, torch_view: torch.Tensor | None = None):
+        self.buffer = buffer
+        self.base_offset = base_offset
+        self.dtype = dtype
+        self.shape = shape
+        self._strides = strides
+        self._torch = torch_view
+        self._storage = buffer._tensor  # the allocation the view aliases (kept alive by the view)
+
+    @property
+    def strides(self) -> tuple[int, ...]:
+        if self._strides is None:
+            self._strides = compute_strides(self.shape, self.dtype)
+        return self._strides
+
+    @property
+    def torch(self) -> torch.Tensor:
+        t = self._torch
+        if t is None:
+            if self.buffer._pending is not None:  # bytes still queued in a deferred batch
+                self.buffer._pending.flush()
+            t = self._torch = _typed(self._storage, self.base_offset, self.dtype, self.shape)
+        return t
 
     @property
     def numel(self) -> int:
@@ -92,6 +118,8 @@ class TensorView:
     def _check_open(self) -> None:
         if self.buffer.released:
             raise UseAfterClose("the buffer backing this view was released")
+        if self.buffer._pending is not None:
+            self.buffer._pending.flush()
 
     def tobytes(self) -> bytes:
         """Little-endian bytes of the viewed region (device -> host copy)."""
@@ -140,9 +168,7 @@ def make_view(buf: DeviceBuffer, base_offset: int, meta: TensorMetadata) -> Tens
         raise OutOfBoundsView(f"view [{base_offset}, {base_offset + extent}) exceeds capacity {buf.capacity}")
     if buf.released:
         raise UseAfterClose("cannot view a released buffer")
-    shape = tuple(meta.shape)
-    t = _typed(buf.tensor, base_offset, meta.dtype, shape)
-    view = TensorView(buf, base_offset, meta.dtype, shape, compute_strides(shape, meta.dtype), t)
+    view = TensorView(buf, base_offset, meta.dtype, tuple(meta.shape))
     buf._live_views.add(view)
     return view
 

@@ -9,6 +9,8 @@ the reference's rules and golden tables.
 from __future__ import annotations
 
 import numpy as np
+import os
+
 import pytest
 
 from conftest import GOLDEN
@@ -118,18 +120,25 @@ def test_engine_team_shares_node_cores(monkeypatch):
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
     assert transfer.engine_team(16) == 4  # floor(0.8 * 40 / 8)
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "64")
-    assert transfer.engine_team(16) == 1
+    assert transfer.engine_team(16) == transfer.MIN_TEAM  # never fewer than MIN_TEAM readers per rank
+    assert transfer.engine_team(2) == 2  # ... unless the cap is lower
 
 
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_bench_cpu_reference_leg(tmp_path, rng, world):
-    """bench.py's reference arm (the CPU port of the reference pipeline) counts
-    exactly the ready bytes of the arm's workload: full tensors at W=1,
-    every rank's Megatron-dim slice at W>1."""
+@pytest.mark.parametrize("kind", ["reference", "port"])
+def test_bench_cpu_reference_leg(tmp_path, rng, world, kind, monkeypatch):
+    """bench.py's reference arm counts exactly the ready bytes of the arm's
+    workload (full tensors at W=1, every rank's Megatron-dim slice at W>1),
+    through the unmodified reference (aggload from baseline/_ref) or, when
+    that is absent, the oracle port; warm and cold passes."""
     import bench
     from paper_2505_23072_b200.format import write_file
 
-    paths, policy, expect = [], {}, 0
+    if kind == "port":
+        monkeypatch.setattr(bench, "reference_package", lambda: None)
+    elif bench.reference_package() is None:
+        pytest.skip("baseline/_ref not installed")
+    paths, policy, keys, expect = [], {}, [], 0
     for f in range(3):
         tensors = {}
         for i in range(4):
@@ -138,13 +147,15 @@ def test_bench_cpu_reference_leg(tmp_path, rng, world):
             name = f"f{f}.t{i}"
             tensors[name] = (DType.BF16, shape, raw)
             policy[name] = (None, 0, 1, 0)[i]
+            keys.append(name)
             expect += len(raw) * (world if (world > 1 and policy[name] is None) else 1)
         p = tmp_path / f"m{f}.safetensors"
         p.write_bytes(write_file(tensors))
         paths.append(p)
-    r = bench.run_cpu_reference(paths, steps=1, warmup=0, world=world, policy=policy)
-    assert r["kind"] == "port" and r["cores"] >= world
-    assert f"{expect} ready tensor bytes" in r["sample"]
+    r = bench.run_cpu_reference(paths, keys, policy, steps=1, warmup=0, cold_steps=1, world=world)
+    assert r["kind"] == kind and r["threads"] >= world and r["host_cores"] == os.cpu_count()
+    assert f"{expect} ready bytes" in r["sample"]
+    assert r["cold"]["residency_before"] == [0.0] or r["cold"]["residency_before"][0] <= 0.01
 
 
 def test_partition_matches_reference_outcomes():

@@ -7,6 +7,9 @@ Variants (one launch = all 291 tensors of the checkpoint unless noted):
   castodd    bf16 -> f16 from a misaligned source
   f32f16     f32 -> f16 (GPT-2 fp32 checkpoint cast)
   pack8      owner-side TP=8 pack of every sharded weight (dim 0 / dim 1 Megatron splits)
+  pack8cast  the same with the bf16 -> f16 cast fused (C5's owner pack)
+  cols8      only the dim-1 (column) shards of pack8: the 2-D TMA tile kernel
+  cols8cast  the same with the cast (tile_cast_kernel)
 
 Prints one JSON line per variant: algorithmic GB/s (read+write) from CUDA
 events around each launch, and the fraction of MEASURED_PEAKS.json hbm_gbs.
@@ -42,13 +45,13 @@ def batches(variant: str, src: torch.Tensor, dst: torch.Tensor, ents):
             sdt, ddt = DType.F16, DType.F32
         elif variant == "bf16f32":
             sdt, ddt = DType.BF16, DType.F32
-        elif variant in ("cast", "castodd"):
+        elif variant in ("cast", "castodd", "pack8cast", "cols8cast"):
             sdt, ddt = DType.BF16, DType.F16
         else:
             sdt, ddt = DType.BF16, DType.BF16
-        if variant == "pack8":
+        if variant.startswith(("pack8", "cols8")):
             d = synth.shard_dim(name, shape)
-            if d is None:
+            if d is None or (variant.startswith("cols8") and d == 0):
                 continue
             for r in range(8):
                 lo, hi = kernels.shard_bounds(shape[d], 8, r)
@@ -66,12 +69,13 @@ def main():
     ap.add_argument("--variants", default="clone,realign,cast,castodd,f32f16,f32f16odd,f16f32,f16f32odd,bf16f32,pack8")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--arch", default="llama2-7b")
+    ap.add_argument("--layers", type=int, default=None)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-    ents = synth.entries(args.arch)
+    ents = synth.entries(args.arch, args.layers)
     for variant in args.variants.split(","):
         if variant in ("f32f16", "f32f16odd"):
             ents_v = [(n, DType.F32, s) for n, _, s in ents]
@@ -92,12 +96,14 @@ def main():
             torch.cuda.synchronize()
             if i >= 2:
                 times.append(sum(a.elapsed_time(b) for a, b, _ in kernels.TIMING))
+                nl = len(kernels.TIMING)
         kernels.TIMING = None
         ms = sorted(times)[len(times) // 2]
         gbs = nbytes / (ms / 1e3) / 1e9
         print(json.dumps({"variant": variant, "descriptors": len(descs), "algorithmic_bytes": nbytes,
                           "ms": round(ms, 4), "GBps": round(gbs, 1), "frac_of_hbm_peak": round(gbs / peak, 4),
-                          "launches": math.ceil(len(descs) / 500)}), flush=True)
+                          "kernels_run_calls": nl, "arch": args.arch,
+                          "layers": args.layers}), flush=True)
         del src, dst
         torch.cuda.empty_cache()
 
