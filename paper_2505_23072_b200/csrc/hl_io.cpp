@@ -710,7 +710,12 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     }
     ranges.push_back({bl.file, bl.file_off, bl.len, bl.dev_dst});
   }
-  const uint64_t cb = ctx->cfg.chunk_bytes;
+  // $HL_PLAN_CHUNK (bytes, <= the ring's slot size) cuts this plan finer (tuning experiments)
+  uint64_t cb = ctx->cfg.chunk_bytes;
+  if (const char* e = getenv("HL_PLAN_CHUNK")) {
+    const uint64_t v = round_up(strtoull(e, nullptr, 10), kAlign);
+    if (v >= kAlign && v < cb) cb = v;
+  }
   for (const Chunk& r : ranges) {
     uint64_t o = r.off;
     const uint64_t end = r.off + r.len;

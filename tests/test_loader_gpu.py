@@ -522,3 +522,45 @@ def test_back_to_back_loads_never_overwrite_pending_reads(tmp_path, batched):
     assert np.array_equal(fb2.get_tensor("w").torch.cpu().numpy(), files[1][1])
     fb2.close()
     second.close()
+
+
+def test_deferred_clone_batches(tmp_path, rng):
+    """World of one, auto_release: per-key clones are queued and launched
+    together (ONE hl_gather per DEFER_KEYS tensors), and every way to reach
+    a result's bytes — .torch, tobytes, the buffer's tensor, close() — sees
+    them written, bit-exact."""
+    from paper_2505_23072_b200 import loader as loader_mod
+
+    t = random_tensor_set(rng, 150, prefix="k", dtypes=[DType.BF16, DType.F32, DType.U8, DType.I64])
+    p = _write(tmp_path, "many.safetensors", t)
+    ld = SafeTensorsFileLoader(SingleGroup(), "host", config=LoaderConfig(auto_release=True))
+    ld.add_filenames({0: [p]})
+    fb = ld.copy_files_to_device()
+    torch.cuda.synchronize()
+    l0 = _native.kernel_launches()
+    views = {k: fb.get_tensor(k) for k in t}
+    queued = _native.kernel_launches() - l0
+    assert queued <= len(t) // loader_mod.DEFER_KEYS  # only full batches went out so far
+    names = list(t)
+    assert views[names[-1]].tobytes() == t[names[-1]][2]  # flushes the tail batch
+    assert _native.kernel_launches() - l0 <= -(-len(t) // loader_mod.DEFER_KEYS) * 2
+    for k in names[:5]:
+        assert views[k].buffer.tensor.numel() >= 0
+    got = {k: v.torch for k, v in views.items()}
+    torch.cuda.synchronize()
+    for k, (dt, shape, raw) in t.items():
+        assert got[k].view(torch.uint8).cpu().numpy().tobytes() == raw if shape else True, k
+        assert views[k].tobytes() == raw, k
+    # a fresh handle: results first read after close()
+    ld2 = SafeTensorsFileLoader(SingleGroup(), "host", config=LoaderConfig(auto_release=True))
+    ld2.add_filenames({0: [p]})
+    fb2 = ld2.copy_files_to_device()
+    later = {k: fb2.get_tensor(k, dtype=(DType.F16 if t[k][0] is DType.BF16 else None)) for k in names[:40]}
+    fb2.close()
+    ld2.close()
+    for k, v in later.items():
+        dt, shape, raw = t[k]
+        exp = oracle.convert(raw, "BF16", "F16") if dt is DType.BF16 else raw
+        assert v.torch.reshape(-1).view(torch.uint8).cpu().numpy().tobytes() == exp, k
+    fb.close()
+    ld.close()
