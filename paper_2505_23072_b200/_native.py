@@ -129,7 +129,7 @@ def load(path: str | os.PathLike | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("HL_LIB", LIB_PATH))  # HL_LIB: tuning builds
         if not p.exists():
             raise NativeUnavailable(
                 f"{p} is missing: build it with `python -m paper_2505_23072_b200._build` "

@@ -873,7 +873,13 @@ constexpr uint32_t kTileBox = 16u << 10;  // bytes of one box (input and output)
 #endif
 constexpr int kTileStages = HL_TILE_STAGES;          // raw copies: 1 thread, 1 CTA per SM
 constexpr int kTileCastStages = HL_TILE_CAST_STAGES;  // casts: in + out stage each, 2 CTAs per SM
-constexpr int kTileConsumerWarps = 8;
+#ifndef HL_TILE_WARPS
+#define HL_TILE_WARPS 8
+#endif
+#ifndef HL_TILE_CAST_CTAS
+#define HL_TILE_CAST_CTAS 2
+#endif
+constexpr int kTileConsumerWarps = HL_TILE_WARPS;
 constexpr int kTileCastThreads = 32 * (1 + kTileConsumerWarps);
 constexpr int kMaxTiles = 96;  // 64 + 96 * 320 = 30784 B of kernel parameters
 
@@ -1313,7 +1319,7 @@ static int launch_tiles(int kind, TileParams& p, cudaStream_t stream) {
       attr_set[dev & 63][kind] = true;
     }
   }
-  const uint64_t cap = (uint64_t)sms * (kind == K_COPY1 ? 1 : 2);
+  const uint64_t cap = (uint64_t)sms * (kind == K_COPY1 ? 1 : HL_TILE_CAST_CTAS);
   const unsigned grid = (unsigned)std::min<uint64_t>(p.total_units, cap);
   tile_kernel_of(kind)<<<grid, kind == K_COPY1 ? 32 : kTileCastThreads, tile_smem(kind), stream>>>(p);
   cudaError_t e = cudaGetLastError();

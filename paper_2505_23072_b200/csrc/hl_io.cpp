@@ -710,8 +710,13 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     }
     ranges.push_back({bl.file, bl.file_off, bl.len, bl.dev_dst});
   }
-  // $HL_PLAN_CHUNK (bytes, <= the ring's slot size) cuts this plan finer (tuning experiments)
+  // Plans under 2 GiB are cut into 2 MiB chunks: the pipeline fill (first reads
+  // before any DMA) and drain are a visible part of a sub-second load (GPT-2's
+  // 0.5 GB: 10.6 vs 11.3 ms engine at 4 MiB; profiles/r02_c1_sweep.jsonl), and
+  // large plans keep the slot size (4 MiB measured best for them).
+  // $HL_PLAN_CHUNK (bytes, <= the ring's slot size) overrides (tuning experiments).
   uint64_t cb = ctx->cfg.chunk_bytes;
+  if (total < (2ull << 30) && cb > (2ull << 20)) cb = 2ull << 20;
   if (const char* e = getenv("HL_PLAN_CHUNK")) {
     const uint64_t v = round_up(strtoull(e, nullptr, 10), kAlign);
     if (v >= kAlign && v < cb) cb = v;

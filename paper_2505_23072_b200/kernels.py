@@ -13,6 +13,7 @@ current CUDA stream with no host synchronisation:
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -49,6 +50,11 @@ def current_stream_ptr(device: torch.device) -> int:
     return _raw_stream(device.index)
 
 
+# Peer pulls (sources in another GPU's memory) run on the LDG/STG warp kernels
+# unless HL_PEER_TMA=1 sends them through the TMA kernels too (the TMA unit then
+# issues the NVLink reads; untested on NVLink here: every gpurun box has one GPU).
+PEER_TMA = os.environ.get("HL_PEER_TMA") == "1"
+
 # Optional launch timing (bench.py): when a list, every run() appends
 # (start_event, end_event, algorithmic_bytes) recorded on the launch stream.
 TIMING: list | None = None
@@ -79,7 +85,7 @@ def run(descs: list[Desc], device: torch.device, peer: bool = False, stream_ptr:
     if torch.cuda.current_device() != device.index:
         with torch.cuda.device(device):
             return run(descs, device, peer, stream_ptr)
-    flags = _native.GATHER_NO_TMA if peer else 0
+    flags = _native.GATHER_NO_TMA if (peer and not PEER_TMA) else 0
     if TIMING is None:
         _native.gather(descs, _raw_stream(device.index) if stream_ptr is None else stream_ptr, flags)
         return

@@ -126,6 +126,16 @@ def golden_job_ipc_batched(rank, world):
     return golden_job(rank, world, plane="ipc", batched=True)
 
 
+def golden_job_ipc_peer_tma(rank, world):
+    """Peer pulls through the TMA kernels (HL_PEER_TMA): key by key and batched."""
+    from paper_2505_23072_b200 import kernels
+
+    kernels.PEER_TMA = True
+    out = golden_job(rank, world, plane="ipc")
+    out.update({(k, "batched"): v for k, v in golden_job(rank, world, plane="ipc", batched=True).items()})
+    return out
+
+
 def golden_job_collective_plane_batched_bcast(rank, world):
     from paper_2505_23072_b200 import loader
 
@@ -133,13 +143,14 @@ def golden_job_collective_plane_batched_bcast(rank, world):
     return golden_job(rank, world, plane="nccl", batched=True)
 
 
-@pytest.mark.parametrize("job", ["collective", "collective_bcast", "ipc"])
+@pytest.mark.parametrize("job", ["collective", "collective_bcast", "ipc", "ipc_peer_tma"])
 @pytest.mark.timeout(600)
 def test_batched_planes_match_reference_loader(job):
     """get_tensors as ONE batch per case: the collective plane's single
     owner-side launch + grouped point-to-point call, and the ipc plane's
     single pull launch, against the reference loader's outputs."""
     fn = {"collective": golden_job_collective_plane_batched, "ipc": golden_job_ipc_batched,
+          "ipc_peer_tma": golden_job_ipc_peer_tma,
           "collective_bcast": golden_job_collective_plane_batched_bcast}[job]
     for rank_result in _run(3, fn):
         assert rank_result and all(rank_result.values()), rank_result
