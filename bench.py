@@ -818,6 +818,9 @@ def main():
                            "engine_ms": stats.engine_seconds * 1e3 if stats else 0.0,
                            "worker_read_s": stats.read_seconds if stats else 0.0,
                            "worker_wait_s": stats.wait_seconds if stats else 0.0,
+                           "engine_setup_ms": stats.setup_seconds * 1e3 if stats else 0.0,
+                           "engine_first_h2d_ms": stats.first_h2d_seconds * 1e3 if stats else 0.0,
+                           "engine_last_h2d_ms": stats.last_h2d_seconds * 1e3 if stats else 0.0,
                            "retrieve_enqueue_ms": (t3 - t2) * 1e3, "retrieve_gpu_ms": retrieve_ms,
                            "drain_ms": wall * 1e3 - (t3 - t0) * 1e3})
         csum = output_checksum(outs) if checksum else None

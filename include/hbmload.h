@@ -129,6 +129,9 @@ typedef struct hl_plan_stats {
   double read_seconds;      /* sum over workers: time inside pread / cuFileRead / pinning */
   double wait_seconds;      /* sum over workers: time waiting for a ring slot's DMA      */
   double submit_seconds;    /* sum over workers: time inside cudaMemcpyAsync/EventRecord */
+  double setup_seconds;     /* plan start -> worker team dispatched (files opened, chunks cut) */
+  double first_h2d_seconds; /* plan start -> first H2D copy submitted                        */
+  double last_h2d_seconds;  /* plan start -> last H2D copy submitted (then the drain)        */
 } hl_plan_stats;
 
 int hl_ctx_create(const hl_config* cfg, hl_ctx** out);

@@ -69,6 +69,9 @@ class hl_plan_stats(C.Structure):
         ("read_seconds", C.c_double),
         ("wait_seconds", C.c_double),
         ("submit_seconds", C.c_double),
+        ("setup_seconds", C.c_double),
+        ("first_h2d_seconds", C.c_double),
+        ("last_h2d_seconds", C.c_double),
     ]
 
 
@@ -236,7 +239,8 @@ class IoEngine:
             "cufile_bytes": st.cufile_bytes, "mmap_bytes": st.mmap_bytes,
             "ring_setup_seconds": st.ring_setup_seconds,
             "read_seconds": st.read_seconds, "wait_seconds": st.wait_seconds,
-            "submit_seconds": st.submit_seconds,
+            "submit_seconds": st.submit_seconds, "setup_seconds": st.setup_seconds,
+            "first_h2d_seconds": st.first_h2d_seconds, "last_h2d_seconds": st.last_h2d_seconds,
             "io_modes": modes, "numa_node": st.numa_node,
         }
 

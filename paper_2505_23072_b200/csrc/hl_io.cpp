@@ -242,6 +242,18 @@ struct PlanRun {
   double ring_setup = 0;
   std::mutex setup_mu;
   std::atomic<uint64_t> read_ns{0}, wait_ns{0}, submit_ns{0};
+  double t0 = 0;                                   // plan start (now_s clock)
+  std::atomic<uint64_t> first_h2d_ns{~0ull}, last_h2d_ns{0};  // since t0
+
+  void note_h2d() {
+    const uint64_t t = (uint64_t)((now_s() - t0) * 1e9);
+    uint64_t f = first_h2d_ns.load(std::memory_order_relaxed);
+    while (t < f && !first_h2d_ns.compare_exchange_weak(f, t)) {
+    }
+    uint64_t l = last_h2d_ns.load(std::memory_order_relaxed);
+    while (t > l && !last_h2d_ns.compare_exchange_weak(l, t)) {
+    }
+  }
 
   void fail(int code, const std::string& msg) {
     std::lock_guard<std::mutex> g(err_mu);
@@ -448,6 +460,7 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
         s.reg = a;
         s.busy = true;
         run->mmap_bytes += c.len;
+        run->note_h2d();
         continue;
       }
       cudaGetLastError();  // registration refused (overlap, limits): copy through the ring
@@ -540,6 +553,7 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
       return;
     }
     s.busy = true;
+    run->note_h2d();
   }
 }
 
@@ -809,6 +823,7 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
   }
 
   PlanRun run;
+  run.t0 = t0;
   run.ctx = ctx;
   run.chunks = &chunks;
   run.files = &files;
@@ -833,6 +848,7 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     run.ring_setup += secs;
   }
   const uint32_t nw = (uint32_t)std::min<size_t>(ctx->cfg.workers, std::max<size_t>(chunks.size(), 1));
+  const double t_dispatch = now_s();
   team_run(ctx, &run, nw);
   close_all();
   if (stats) {
@@ -854,6 +870,9 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     stats->read_seconds = run.read_ns.load() * 1e-9;
     stats->wait_seconds = run.wait_ns.load() * 1e-9;
     stats->submit_seconds = run.submit_ns.load() * 1e-9;
+    stats->setup_seconds = t_dispatch - t0;
+    stats->first_h2d_seconds = run.first_h2d_ns.load() == ~0ull ? 0.0 : run.first_h2d_ns.load() * 1e-9;
+    stats->last_h2d_seconds = run.last_h2d_ns.load() * 1e-9;
   }
   if (run.err_code != HL_OK) return set_error(run.err_code, "%s", run.err_msg.c_str());
   return HL_OK;

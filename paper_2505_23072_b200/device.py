@@ -142,7 +142,7 @@ class DeviceBuffer:
         self.backend = pool.backend
         self.refcount = 0
         self.released = False
-        self._live_views: weakref.WeakSet = weakref.WeakSet()
+        self._views: weakref.WeakSet | None = None  # created with the first view (most buffers get one)
         self._pending = None  # a deferred retrieval batch that still has to write this buffer
 
     @property
@@ -178,7 +178,12 @@ class DeviceBuffer:
         return self.tensor[off : off + length].cpu().numpy().tobytes()
 
     def live_view_count(self) -> int:
-        return len(self._live_views)
+        return len(self._views) if self._views is not None else 0
+
+    def _add_view(self, view) -> None:
+        if self._views is None:
+            self._views = weakref.WeakSet()
+        self._views.add(view)
 
     def release(self, *, force: bool = False, to_pool: bool = True) -> None:
         self.pool.release(self, force=force, to_pool=to_pool)

@@ -169,7 +169,7 @@ def make_view(buf: DeviceBuffer, base_offset: int, meta: TensorMetadata) -> Tens
     if buf.released:
         raise UseAfterClose("cannot view a released buffer")
     view = TensorView(buf, base_offset, meta.dtype, tuple(meta.shape))
-    buf._live_views.add(view)
+    buf._add_view(view)
     return view
 
 

@@ -40,7 +40,7 @@ def test_struct_sizes_match_header_layout():
     assert C.sizeof(_native.hl_desc) == 48
     assert C.sizeof(_native.hl_block) == 32
     assert C.sizeof(_native.hl_config) == 32
-    assert C.sizeof(_native.hl_plan_stats) == 96
+    assert C.sizeof(_native.hl_plan_stats) == 120
 
 
 def test_version_and_conversion_table():
