@@ -10,7 +10,7 @@ D=${HL_BENCH_DIR:-/tmp/hl_bench}
 T=${T:-1200}
 run() { local name=$1; shift; timeout $T "$@" > gpurun_out/cfg_$name.log 2>&1; echo "$name exit $?"; }
 run c1 python bench.py --arch gpt2 --steps 5 --warmup 3
-run c1_odd_gds python bench.py --arch gpt2 --header odd --backend gds --steps 5 --warmup 3 --baselines 0
+run c1_odd_gds python bench.py --arch gpt2 --header odd --backend gds --steps 5 --warmup 3
 run c1_f16 python bench.py --arch gpt2 --cast F16 --steps 5 --warmup 3
 rm -rf $D/gpt2-*
 run c2 python bench.py --steps 5 --warmup 3
@@ -18,12 +18,17 @@ rm -rf $D/llama2-7b-*
 run c3 python bench.py --arch llama2-13b --steps 3 --warmup 3
 for n in 2 4; do
   HL_SHARE_GPU=1 run c3_tp$n python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
-      --master-port $((29700 + n)) bench.py --arch llama2-13b --gpus $n --steps 3 --warmup 3 --quick
+      --master-port $((29700 + n)) bench.py --arch llama2-13b --gpus $n --steps 3 --warmup 3 --quick --data-plane ipc
 done
 rm -rf $D/llama2-13b-*
-run c4_l24 python bench.py --arch llama2-70b --layers 24 --steps 3 --warmup 3 --baselines 0
+run c4_l24 python bench.py --arch llama2-70b --layers 24 --steps 3 --warmup 3
+# C4 shape at TP=8 (8 ranks sharing the GPU): both data planes (NCCL plane = gloo-staged here)
+HL_SHARE_GPU=1 run c4_l4_tp8 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \
+    --master-port 29718 bench.py --arch llama2-70b --layers 4 --gpus 8 --steps 2 --warmup 2 --quick --cold-steps 1
 rm -rf $D/llama2-70b-*
 run c5_l8_f16 python bench.py --arch bloom-176b --layers 8 --cast F16 --steps 3 --warmup 3
+HL_SHARE_GPU=1 run c5_l2_tp8_f16 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \
+    --master-port 29728 bench.py --arch bloom-176b --layers 2 --cast F16 --gpus 8 --steps 2 --warmup 2 --quick --cold-steps 1
 rm -rf $D/bloom-176b-*
 df -h /tmp > gpurun_out/cfg_df.txt
 exit 0
