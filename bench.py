@@ -896,6 +896,7 @@ def main():
                 "seconds_to_ready": round(med / 1e3, 3), "steps": args.cold_steps,
                 "residency_before": resid_before,
                 "io_modes": sorted(st.io_modes) if st else None,
+                "io_threads": st.io_threads if st else None,
                 "direct_bytes": st.direct_bytes if st else None,
                 "buffered_bytes": st.buffered_bytes if st else None}
         warm_cache(mapping[rank])

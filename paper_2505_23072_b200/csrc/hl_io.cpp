@@ -21,7 +21,8 @@
 // The ring is one pinned region per context (huge-page backed, first-touched
 // on the GPU's NUMA node, see ensure_ring_memory), allocated before the first
 // plan's workers start and reused by every later plan; its cost is reported in
-// hl_plan_stats.ring_setup_seconds.
+// hl_plan_stats.ring_setup_seconds. A plan that is mostly cold (O_DIRECT) runs
+// on a larger team (cold_workers) whose extra slots get a second region.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdlib.h>
@@ -198,9 +199,17 @@ struct hl_ctx {
   std::vector<WorkerRing> rings;
   bool ring_ready = false;
   uint64_t slot_bytes = 0;
-  uint8_t* ring_mem = nullptr;  // every worker's slots, one pinned region
-  uint64_t ring_bytes = 0;
-  bool ring_registered = false;  // cudaHostRegister'ed malloc (else cudaHostAlloc)
+  // Pinned slot memory: region i serves workers [w0, w1) (the warm team first,
+  // the extra cold readers in a second region allocated by the first cold plan).
+  struct RingRegion {
+    uint8_t* mem;
+    uint64_t bytes;
+    bool registered;  // cudaHostRegister'ed malloc (else cudaHostAlloc)
+    uint32_t w0, w1;
+  };
+  std::vector<RingRegion> regions;
+  uint32_t ring_workers = 0;  // workers whose slots have memory
+  uint32_t cold_workers = 0;  // team size for plans that are mostly O_DIRECT reads
   std::mutex mu;  // one plan at a time per context
   cudaEvent_t order_ev = nullptr;  // hl_execute_plan_after: the caller's stream position
   // Persistent worker team (threads live as long as the context): a plan is a
@@ -292,10 +301,12 @@ bool pread_full(int fd, uint8_t* buf, uint64_t len, uint64_t off, uint64_t* got,
 // 144 MiB, vs 74 ms for 36 separate cudaHostAlloc calls — and slot-by-slot
 // allocation during the first load stalled behind the in-flight copies (first
 // load 0.73 s vs 0.27 s steady; profiles/r01_first_load.jsonl).
-int ensure_ring_memory(hl_ctx* ctx, double* seconds) {
-  if (ctx->ring_mem) return HL_OK;
+int ensure_ring_memory(hl_ctx* ctx, uint32_t nworkers, double* seconds) {
+  if (ctx->ring_workers >= nworkers) return HL_OK;
   const double t0 = now_s();
-  const uint64_t bytes = round_up((uint64_t)ctx->cfg.workers * ctx->cfg.slots_per_worker * ctx->slot_bytes, 2ull << 20);
+  const uint32_t w0 = ctx->ring_workers;
+  const uint64_t bytes =
+      round_up((uint64_t)(nworkers - w0) * ctx->cfg.slots_per_worker * ctx->slot_bytes, 2ull << 20);
   void* m = nullptr;
   bool registered = false;
   if (posix_memalign(&m, 2ull << 20, bytes) == 0) {
@@ -326,9 +337,8 @@ int ensure_ring_memory(hl_ctx* ctx, double* seconds) {
       return set_error(HL_ENOMEM, "pinned ring of %llu bytes: %s", (unsigned long long)bytes, cudaGetErrorString(e));
     }
   }
-  ctx->ring_mem = (uint8_t*)m;
-  ctx->ring_bytes = bytes;
-  ctx->ring_registered = registered;
+  ctx->regions.push_back({(uint8_t*)m, bytes, registered, w0, nworkers});
+  ctx->ring_workers = nworkers;
   *seconds = now_s() - t0;
   return HL_OK;
 }
@@ -348,9 +358,13 @@ int ensure_ring(hl_ctx* ctx, WorkerRing& r) {
 
 int ensure_slot(hl_ctx* ctx, uint32_t w, uint32_t k, Slot& s) {
   if (s.host) return HL_OK;
-  if (!ctx->ring_mem) return set_error(HL_ENOMEM, "pinned ring not allocated");
-  s.host = ctx->ring_mem + ((uint64_t)w * ctx->cfg.slots_per_worker + k) * ctx->slot_bytes;
-  return HL_OK;
+  for (const auto& r : ctx->regions) {
+    if (w >= r.w0 && w < r.w1) {
+      s.host = r.mem + ((uint64_t)(w - r.w0) * ctx->cfg.slots_per_worker + k) * ctx->slot_bytes;
+      return HL_OK;
+    }
+  }
+  return set_error(HL_ENOMEM, "pinned ring not allocated for worker %u", w);
 }
 
 static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring);
@@ -583,7 +597,7 @@ void team_thread(hl_ctx* ctx, uint32_t w) {
 
 // Run `run` on the first `n` team threads (spawned once per context) and wait.
 void team_run(hl_ctx* ctx, PlanRun* run, uint32_t n) {
-  while (ctx->team.size() < ctx->cfg.workers) {
+  while (ctx->team.size() < n) {
     const uint32_t w = (uint32_t)ctx->team.size();
     ctx->team.emplace_back(team_thread, ctx, w);
   }
@@ -650,7 +664,14 @@ extern "C" int hl_ctx_create(const hl_config* cfg, hl_ctx** out) {
   ctx->cfg.chunk_bytes = round_up(ctx->cfg.chunk_bytes, kAlign);
   if (ctx->cfg.slots_per_worker == 0) ctx->cfg.slots_per_worker = 3;
   ctx->slot_bytes = ctx->cfg.chunk_bytes + 2 * kAlign;  // O_DIRECT head/tail slack
-  ctx->rings.resize(ctx->cfg.workers);
+  // Cold reads are storage-latency bound, not CPU bound: more requests in flight
+  // raise the rate (O_DIRECT 4 MiB preads on the box: 16 threads 3.8 GB/s, 32
+  // threads 4.8; profiles/r02_bench_n1_v4.json storage_probe). Plans whose bytes
+  // are mostly not in the page cache run on this larger team ($HL_COLD_WORKERS).
+  uint32_t cold = 32;
+  if (const char* e = getenv("HL_COLD_WORKERS")) cold = (uint32_t)std::max(1L, std::min(strtol(e, nullptr, 10), 64L));
+  ctx->cold_workers = std::max(ctx->cfg.workers, cold);
+  ctx->rings.resize(ctx->cold_workers);
   *out = ctx;
   return HL_OK;
 }
@@ -679,12 +700,12 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
     }
     if (r.stream) cudaStreamDestroy(r.stream);
   }
-  if (ctx->ring_mem) {
-    if (ctx->ring_registered) {
-      cudaHostUnregister(ctx->ring_mem);
-      free(ctx->ring_mem);
+  for (const auto& r : ctx->regions) {
+    if (r.registered) {
+      cudaHostUnregister(r.mem);
+      free(r.mem);
     } else {
-      cudaFreeHost(ctx->ring_mem);
+      cudaFreeHost(r.mem);
     }
   }
   delete ctx;
@@ -838,16 +859,43 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     }
     run.order_ev = ctx->order_ev;
   }
+  // Team size: the warm team, or the cold readers when most of the plan's bytes
+  // will be read with O_DIRECT (direct mode; auto mode with < half resident).
+  uint32_t team = ctx->cfg.workers;
+  if (ctx->cold_workers > team && total > 0) {
+    // estimate from 64 sampled pages per file (mincore of one page each: cheap)
+    std::vector<uint64_t> plan_bytes(n_files, 0);
+    for (const Chunk& c : chunks) plan_bytes[c.file] += c.len;
+    double cold_bytes = 0;
+    for (uint32_t i = 0; i < n_files; ++i) {
+      const FileState& f = files[i];
+      if (!plan_bytes[i]) continue;
+      if (f.mode == HL_IO_DIRECT && f.dfd >= 0) {
+        cold_bytes += (double)plan_bytes[i];
+      } else if (f.mode == HL_IO_AUTO && f.probe && f.size >= kAlign) {
+        const uint64_t pages = f.size / kAlign;
+        const uint64_t n = std::min<uint64_t>(64, pages);
+        uint64_t res = 0;
+        for (uint64_t q = 0; q < n; ++q) {
+          unsigned char v = 0;
+          const uint64_t pg = (2 * q + 1) * pages / (2 * n);
+          if (mincore(f.probe + pg * kAlign, kAlign, &v) == 0) res += v & 1;
+        }
+        cold_bytes += (double)plan_bytes[i] * (double)(n - res) / (double)n;
+      }
+    }
+    if (cold_bytes * 2 > (double)total) team = ctx->cold_workers;
+  }
+  const uint32_t nw = (uint32_t)std::min<size_t>(team, std::max<size_t>(chunks.size(), 1));
   {
     double secs = 0;
-    int rc = ensure_ring_memory(ctx, &secs);
+    int rc = ensure_ring_memory(ctx, nw, &secs);
     if (rc) {
       close_all();
       return rc;
     }
     run.ring_setup += secs;
   }
-  const uint32_t nw = (uint32_t)std::min<size_t>(ctx->cfg.workers, std::max<size_t>(chunks.size(), 1));
   const double t_dispatch = now_s();
   team_run(ctx, &run, nw);
   close_all();

@@ -197,3 +197,22 @@ def test_worker_team_is_persistent_and_pinned(blob):
         assert all(a == set(cpus) for a in new.values())
     eng.close()
     assert not set(new) & set(team())  # joined on close
+
+
+def test_cold_plans_run_on_the_cold_team(blob):
+    """A plan that is mostly O_DIRECT reads (direct mode, or auto with the file
+    dropped from the page cache) runs on the larger cold-reader team; a resident
+    one keeps the configured team. Bytes are exact either way."""
+    path, data = blob
+    n = 32 << 20
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+    eng = _native.IoEngine(0, workers=4, chunk_bytes=1 << 20, io_mode="auto")
+    path.read_bytes()
+    warm = eng.execute([str(path)], [(0, 0, 0, n, dst.data_ptr())], after_stream=0)
+    assert warm["workers"] == 4 and np.array_equal(dst.cpu().numpy(), data[:n])
+    _native.drop_cache(str(path))
+    dst.zero_()
+    cold = eng.execute([str(path)], [(0, 0, 0, n, dst.data_ptr())], after_stream=0)
+    assert cold["workers"] > 4 and "direct" in cold["io_modes"], cold
+    assert np.array_equal(dst.cpu().numpy(), data[:n])
+    eng.close()
