@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define HL_ABI_VERSION 2  /* 2: hl_execute_plan_after, hl_ctx_cpus, hl_topology_resolve, stats.numa_node */
+#define HL_ABI_VERSION 2  /* 2: hl_execute_plan_after/_async, hl_ctx_cpus, hl_topology_resolve, stats.numa_node */
 
 /* ---- status codes (errors.py class in brackets) ---------------------------- */
 enum hl_status {
@@ -155,6 +155,17 @@ int hl_execute_plan(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
  * kernels queued on `stream` still read is not overwritten before they ran.
  * NULL = the legacy default stream. The loader always uses this entry. */
 int hl_execute_plan_after(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
+                          const hl_block* blocks, uint32_t n_blocks, void* stream,
+                          hl_plan_stats* stats);
+
+/* hl_execute_plan_after that returns once every byte has been read from
+ * storage and its H2D copy submitted, instead of draining the copies: `stream`
+ * is made to wait for all of them (cudaStreamWaitEvent), so work enqueued on
+ * it afterwards — kernels, stream-ordered frees, a D2H read — sees the bytes,
+ * while the host goes on (the drain of the last copies overlaps the caller's
+ * next steps). Host access to the destinations needs a sync of `stream`.
+ * Read errors are reported here as before. */
+int hl_execute_plan_async(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
                           const hl_block* blocks, uint32_t n_blocks, void* stream,
                           hl_plan_stats* stats);
 

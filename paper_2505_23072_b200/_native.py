@@ -103,6 +103,8 @@ SIGNATURES = {
                                   C.POINTER(hl_block), C.c_uint32, C.POINTER(hl_plan_stats)]),
     "hl_execute_plan_after": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32,
                                         C.POINTER(hl_block), C.c_uint32, C.c_void_p, C.POINTER(hl_plan_stats)]),
+    "hl_execute_plan_async": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32,
+                                        C.POINTER(hl_block), C.c_uint32, C.c_void_p, C.POINTER(hl_plan_stats)]),
     "hl_ctx_cpus": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_uint32)]),
     "hl_topology_resolve": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                       C.c_uint32, C.POINTER(C.c_uint32)]),
@@ -218,11 +220,13 @@ class IoEngine:
         self.config = {f: getattr(eff, f) for f, _ in hl_config._fields_}
 
     def execute(self, paths: list[str], blocks: list[tuple[int, int, int, int, int]],
-                after_stream: int | None = None) -> dict:
+                after_stream: int | None = None, async_tail: bool = False) -> dict:
         """blocks: (file_index, worker_hint, file_off, len, dev_dst). Blocking.
         ``after_stream`` (a cudaStream_t as int, 0 = legacy default): the
         engine's HBM writes wait for everything already queued on it
-        (hl_execute_plan_after); None = unordered (hl_execute_plan)."""
+        (hl_execute_plan_after); None = unordered (hl_execute_plan).
+        ``async_tail``: return once every copy is submitted, with the stream
+        waiting for their completion (hl_execute_plan_async)."""
         lib = self._lib
         cpaths = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
         arr = (hl_block * len(blocks))(*[hl_block(*b) for b in blocks])
@@ -230,8 +234,8 @@ class IoEngine:
         if after_stream is None:
             check(lib.hl_execute_plan(self._h, cpaths, len(paths), arr, len(blocks), C.byref(st)))
         else:
-            check(lib.hl_execute_plan_after(self._h, cpaths, len(paths), arr, len(blocks),
-                                            C.c_void_p(after_stream), C.byref(st)))
+            fn = lib.hl_execute_plan_async if async_tail else lib.hl_execute_plan_after
+            check(fn(self._h, cpaths, len(paths), arr, len(blocks), C.c_void_p(after_stream), C.byref(st)))
         modes = [name for bit, name in IO_MODE_NAMES.items() if st.io_mode_used & (1 << bit)]
         return {
             "bytes": st.bytes, "seconds": st.seconds, "workers": st.workers, "blocks": st.blocks,

@@ -190,6 +190,7 @@ struct Slot {
 struct WorkerRing {
   std::vector<Slot> slots;
   cudaStream_t stream = nullptr;
+  cudaEvent_t tail = nullptr;  // hl_execute_plan_async: this worker's last copy of the plan
   size_t next = 0;
 };
 
@@ -240,6 +241,8 @@ struct FileState {
 struct PlanRun {
   hl_ctx* ctx;
   cudaEvent_t order_ev = nullptr;  // every H2D waits for it (caller's stream position)
+  bool async_tail = false;         // hand the copies' completion to `after` instead of draining
+  cudaStream_t after = nullptr;
   const std::vector<Chunk>* chunks;
   std::vector<FileState>* files;
   std::atomic<size_t> cursor{0};
@@ -348,6 +351,8 @@ int ensure_ring(hl_ctx* ctx, WorkerRing& r) {
   if (!r.slots.empty()) return HL_OK;
   cudaError_t e = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return set_error(HL_ECUDA, "stream create: %s", cudaGetErrorString(e));
+  e = cudaEventCreateWithFlags(&r.tail, cudaEventDisableTiming);
+  if (e != cudaSuccess) return set_error(HL_ECUDA, "event create: %s", cudaGetErrorString(e));
   r.slots.resize(ctx->cfg.slots_per_worker);
   for (auto& s : r.slots) {
     e = cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming);
@@ -396,7 +401,19 @@ void worker_main(PlanRun* run, uint32_t w) {
     }
   }
   worker_loop(run, w, ring);
-  // Drain on every exit, failed or not: the caller frees (or reuses) the
+  bool pinned = false;  // page-cache ranges pinned for in-flight copies are unpinned only after them
+  for (const auto& s : ring.slots) pinned |= s.reg != nullptr;
+  if (run->async_tail && !pinned && !run->failed.load()) {
+    // Completion goes to the caller's stream: it waits for this worker's last
+    // copy, so every kernel enqueued there afterwards sees the bytes, and the
+    // caller's stream-ordered frees cannot recycle a destination under a copy.
+    // The slots stay busy; their next user waits on their events.
+    cudaError_t e = cudaEventRecord(ring.tail, ring.stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(run->after, ring.tail, 0);
+    if (e == cudaSuccess) return;
+    run->fail(HL_ECUDA, std::string("completion handoff: ") + cudaGetErrorString(e));
+  }
+  // Drain on every other exit, failed or not: the caller frees (or reuses) the
   // destination buffers as soon as hl_execute_plan returns, so no DMA of this
   // worker may still be in flight, and no page-cache range may stay pinned.
   cudaError_t e = cudaStreamSynchronize(ring.stream);
@@ -695,6 +712,7 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
   if (ctx->order_ev) cudaEventDestroy(ctx->order_ev);
   for (auto& r : ctx->rings) {
     if (r.stream) cudaStreamSynchronize(r.stream);
+    if (r.tail) cudaEventDestroy(r.tail);
     for (auto& s : r.slots) {
       if (s.ev) cudaEventDestroy(s.ev);
     }
@@ -713,7 +731,8 @@ extern "C" int hl_ctx_destroy(hl_ctx* ctx) {
 }
 
 static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, const hl_block* blocks,
-                   uint32_t n_blocks, bool ordered, cudaStream_t after, hl_plan_stats* stats) {
+                   uint32_t n_blocks, bool ordered, cudaStream_t after, hl_plan_stats* stats,
+                   bool async_tail = false) {
   clear_error();
   if (!ctx) return set_error(HL_EINVAL, "null context");
   if (n_blocks && (!blocks || !paths)) return set_error(HL_EINVAL, "null blocks or paths");
@@ -858,6 +877,8 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
       return set_error(HL_ECUDA, "ordering after the caller's stream: %s", cudaGetErrorString(e));
     }
     run.order_ev = ctx->order_ev;
+    run.async_tail = async_tail;
+    run.after = after;
   }
   // Team size: the warm team, or the cold readers when most of the plan's bytes
   // will be read with O_DIRECT (direct mode; auto mode with < half resident).
@@ -935,6 +956,12 @@ extern "C" int hl_execute_plan_after(hl_ctx* ctx, const char* const* paths, uint
                                      const hl_block* blocks, uint32_t n_blocks, void* stream,
                                      hl_plan_stats* stats) {
   return execute(ctx, paths, n_files, blocks, n_blocks, true, (cudaStream_t)stream, stats);
+}
+
+extern "C" int hl_execute_plan_async(hl_ctx* ctx, const char* const* paths, uint32_t n_files,
+                                     const hl_block* blocks, uint32_t n_blocks, void* stream,
+                                     hl_plan_stats* stats) {
+  return execute(ctx, paths, n_files, blocks, n_blocks, true, (cudaStream_t)stream, stats, true);
 }
 
 extern "C" int hl_transfer_from_file(hl_ctx* ctx, const char* path, uint64_t file_off, uint64_t len, void* dev_dst) {

@@ -216,3 +216,25 @@ def test_cold_plans_run_on_the_cold_team(blob):
     assert cold["workers"] > 4 and "direct" in cold["io_modes"], cold
     assert np.array_equal(dst.cpu().numpy(), data[:n])
     eng.close()
+
+
+def test_async_plans_hand_completion_to_the_stream(blob):
+    """hl_execute_plan_async returns once the copies are submitted; work
+    enqueued on the stream afterwards (here a clone, no host sync in between)
+    sees every byte, also across back-to-back plans that reuse the ring slots
+    while earlier copies may still be in flight."""
+    path, data = blob
+    n = 12 << 20
+    eng = _native.IoEngine(0, workers=3, chunk_bytes=1 << 20, io_mode="buffered")
+    s = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for i in range(6):
+        off = (i * 5 << 20) % (data.size - n)
+        dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+        eng.execute([str(path)], [(0, 0, off, n, dst.data_ptr())], after_stream=s, async_tail=True)
+        outs.append((off, dst.clone()))  # enqueued behind the plan's copies
+        del dst  # stream-ordered free: must not be recycled under an in-flight copy
+    torch.cuda.synchronize()
+    for off, got in outs:
+        assert np.array_equal(got.cpu().numpy(), data[off:off + n]), off
+    eng.close()
