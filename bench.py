@@ -883,6 +883,9 @@ def main():
     e2e, e2e_med, launches_e2e, clk = primary
     value = job_bytes / (e2e_med / 1e3) / 1e9
 
+    io = None
+    if rank == 0 and world == 1 and not args.quick:
+        io = io_probes(paths, local)  # storage probe right before the cold leg (same cache state)
     cold = None
     if args.cold_steps:
         cms, resid_before, st = [], [], None
@@ -901,7 +904,7 @@ def main():
                 "buffered_bytes": st.buffered_bytes if st else None}
         warm_cache(mapping[rank])
 
-    io = cpu = libs = fresh = None
+    cpu = libs = fresh = None
     if rank == 0 and world == 1 and not args.quick:
         fresh = e2e_fresh_process(paths, local, args.backend, job_bytes) if cast is None else None
         if args.baselines:
@@ -909,7 +912,6 @@ def main():
         if args.cpu_baseline:
             cpu = run_cpu_reference(paths, keys, policy, steps=1, warmup=0, cold_steps=1 if args.cold_steps else 0,
                                     cast=cast)
-        io = io_probes(paths, local)
         io["e2e_frac_of_h2d"] = round(value / io["h2d_gbs"], 4)
         if cold and io.get("storage_gbs"):
             io["cold_frac_of_storage"] = round(cold["value"] / io["storage_gbs"], 4)

@@ -201,10 +201,14 @@ int main(int argc, char** argv) {
   }
   threads(16, 16 << 20);
   threads(32, 4 << 20);
+  threads(48, 4 << 20);
+  threads(32, 8 << 20);
   threads(64, 1 << 20);
   threads(64, 4 << 20);
   uring(32, 1 << 20);
   uring(64, 1 << 20);
+  uring(64, 2 << 20);
+  uring(128, 1 << 20);
   uring(128, 512 << 10);
   uring(64, 4 << 20);
   return 0;
