@@ -170,6 +170,27 @@ def _entry(name: str, e) -> TensorMetadata:
     return TensorMetadata(name, dtype, tuple(shape), (offs[0], offs[1]))
 
 
+_BY_TAG = {m.value: m for m in DType}
+
+
+def _entry_fast(name: str, e) -> TensorMetadata:
+    """``_entry`` for the well-formed case in a few type checks; anything
+    unusual goes to ``_entry``, which raises the exact error (same classes,
+    same check order)."""
+    if type(e) is dict:
+        tag, shape, offs = e.get("dtype"), e.get("shape"), e.get("data_offsets")
+        dtype = _BY_TAG.get(tag) if type(tag) is str else None
+        if dtype is not None and type(shape) is list and type(offs) is list and len(offs) == 2:
+            b, n = offs
+            if type(b) is int and type(n) is int and b >= 0 and n >= 0:
+                for d in shape:
+                    if type(d) is not int or d < 0:
+                        break
+                else:
+                    return TensorMetadata(name, dtype, tuple(shape), (b, n))
+    return _entry(name, e)
+
+
 def _layout(doc: bytes, header_len: int) -> FileHeader:
     try:
         obj = json.loads(doc.decode("utf-8"), object_pairs_hook=_no_dup_pairs)
@@ -189,7 +210,7 @@ def _layout(doc: bytes, header_len: int) -> FileHeader:
                 raise MalformedJson("__metadata__ must map strings to strings")
             meta = dict(e)
         else:
-            tensors[name] = _entry(name, e)
+            tensors[name] = _entry_fast(name, e)
     return FileHeader(header_len, tensors, meta)
 
 
