@@ -429,6 +429,19 @@ def run_cpu_reference(paths, keys, policy, steps: int, warmup: int, cold_steps: 
         tc = statistics.median(cold)
         out["cold"] = {"value": round(ready / tc / 1e9, 4), "unit": "GB/s", "seconds": round(tc, 4),
                        "residency_before": resid, "steps": cold_steps}
+    if agg is not None and world == 1 and cast is None:
+        # the reference's own naive baseline (ref reference.py:80-91: per-tensor seek/read ->
+        # host array -> device-style copy, one tensor at a time), one warm pass
+        from aggload.reference import naive_sequential_load
+
+        t0 = time.perf_counter()
+        got = naive_sequential_load(paths)
+        tn = time.perf_counter() - t0
+        nb = sum(a.nbytes for a in got.values())
+        del got
+        out["naive_sequential"] = {"value": round(nb / tn / 1e9, 4), "unit": "GB/s", "seconds": round(tn, 4),
+                                   "call": "aggload.reference.naive_sequential_load", "threads": 1,
+                                   "page_cache": "warm"}
     return out
 
 

@@ -679,7 +679,10 @@ extern "C" int hl_ctx_create(const hl_config* cfg, hl_ctx** out) {
   }
   if (ctx->cfg.chunk_bytes == 0) ctx->cfg.chunk_bytes = 16ull << 20;
   ctx->cfg.chunk_bytes = round_up(ctx->cfg.chunk_bytes, kAlign);
-  if (ctx->cfg.slots_per_worker == 0) ctx->cfg.slots_per_worker = 3;
+  if (ctx->cfg.slots_per_worker == 0) {
+    ctx->cfg.slots_per_worker = 3;
+    if (const char* e = getenv("HL_ENGINE_SLOTS")) ctx->cfg.slots_per_worker = (uint32_t)std::max(1L, std::min(strtol(e, nullptr, 10), 16L));
+  }
   ctx->slot_bytes = ctx->cfg.chunk_bytes + 2 * kAlign;  // O_DIRECT head/tail slack
   // Cold reads are storage-latency bound, not CPU bound: more requests in flight
   // raise the rate (O_DIRECT 4 MiB preads on the box: 16 threads 3.8 GB/s, 32
@@ -764,27 +767,6 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     }
     ranges.push_back({bl.file, bl.file_off, bl.len, bl.dev_dst});
   }
-  // Plans under 2 GiB are cut into 2 MiB chunks: the pipeline fill (first reads
-  // before any DMA) and drain are a visible part of a sub-second load (GPT-2's
-  // 0.5 GB: 10.6 vs 11.3 ms engine at 4 MiB; profiles/r02_c1_sweep.jsonl), and
-  // large plans keep the slot size (4 MiB measured best for them).
-  // $HL_PLAN_CHUNK (bytes, <= the ring's slot size) overrides (tuning experiments).
-  uint64_t cb = ctx->cfg.chunk_bytes;
-  if (total < (2ull << 30) && cb > (2ull << 20)) cb = 2ull << 20;
-  if (const char* e = getenv("HL_PLAN_CHUNK")) {
-    const uint64_t v = round_up(strtoull(e, nullptr, 10), kAlign);
-    if (v >= kAlign && v < cb) cb = v;
-  }
-  for (const Chunk& r : ranges) {
-    uint64_t o = r.off;
-    const uint64_t end = r.off + r.len;
-    while (o < end) {
-      const uint64_t n = std::min<uint64_t>(round_down(o, cb) + cb, end) - o;
-      chunks.push_back({r.file, o, n, r.dst + (o - r.off)});
-      o += n;
-    }
-  }
-
   // open files, pick the read mode per file
   std::vector<FileState> files(n_files);
   auto close_all = [&]() {
@@ -854,7 +836,7 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     f.mode = (int)mode;
     mode_mask |= 1u << mode;
   }
-  for (const Chunk& c : chunks) {
+  for (const Chunk& c : ranges) {
     if (c.off + c.len > files[c.file].size) {
       close_all();
       return set_error(HL_EIO, "range [%llu, %llu) past end of %s (%llu bytes)", (unsigned long long)c.off,
@@ -867,7 +849,7 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
   run.ctx = ctx;
   run.chunks = &chunks;
   run.files = &files;
-  if (ordered && !chunks.empty()) {
+  if (ordered && !ranges.empty()) {
     cudaError_t e = ctx->order_ev ? cudaSuccess : cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(ctx->order_ev, after);
     // cuFile writes HBM from the host thread, outside any stream: wait here
@@ -886,7 +868,7 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
   if (ctx->cold_workers > team && total > 0) {
     // estimate from 64 sampled pages per file (mincore of one page each: cheap)
     std::vector<uint64_t> plan_bytes(n_files, 0);
-    for (const Chunk& c : chunks) plan_bytes[c.file] += c.len;
+    for (const Chunk& c : ranges) plan_bytes[c.file] += c.len;
     double cold_bytes = 0;
     for (uint32_t i = 0; i < n_files; ++i) {
       const FileState& f = files[i];
@@ -906,6 +888,32 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
       }
     }
     if (cold_bytes * 2 > (double)total) team = ctx->cold_workers;
+  }
+  const bool cold_plan = team > ctx->cfg.workers;
+  // Chunk size. Plans under 2 GiB are cut into 2 MiB chunks: the pipeline fill
+  // (first reads before any DMA) and drain are a visible part of a sub-second
+  // load (GPT-2's 0.5 GB: 10.6 vs 11.3 ms engine at 4 MiB;
+  // profiles/r02_c1_sweep.jsonl); large warm plans keep the slot size (4 MiB
+  // measured best for them). Cold plans read 1 MiB O_DIRECT requests: the
+  // storage rate follows the requests in flight, not their size (32 readers:
+  // 1 MiB 5.87 GB/s, 2 MiB 5.27, 4 MiB 5.12 cold e2e on the same box, whose best
+  // storage probe was io_uring depth 32 x 1 MiB; profiles/r02_cold_sweep.jsonl).
+  // $HL_PLAN_CHUNK / $HL_COLD_CHUNK (bytes, <= the ring's slot size) override.
+  uint64_t cb = ctx->cfg.chunk_bytes;
+  if (total < (2ull << 30) && cb > (2ull << 20)) cb = 2ull << 20;
+  if (cold_plan && cb > (1ull << 20)) cb = 1ull << 20;
+  if (const char* e = getenv(cold_plan ? "HL_COLD_CHUNK" : "HL_PLAN_CHUNK")) {
+    const uint64_t v = round_up(strtoull(e, nullptr, 10), kAlign);
+    if (v >= kAlign && v <= ctx->cfg.chunk_bytes) cb = v;
+  }
+  for (const Chunk& r : ranges) {
+    uint64_t o = r.off;
+    const uint64_t end = r.off + r.len;
+    while (o < end) {
+      const uint64_t n = std::min<uint64_t>(round_down(o, cb) + cb, end) - o;
+      chunks.push_back({r.file, o, n, r.dst + (o - r.off)});
+      o += n;
+    }
   }
   const uint32_t nw = (uint32_t)std::min<size_t>(team, std::max<size_t>(chunks.size(), 1));
   {
