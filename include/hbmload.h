@@ -113,6 +113,9 @@ typedef struct hl_block {
   uint64_t dev_dst;
 } hl_block;
 
+/* io_mode_used bit: some O_DIRECT reads were issued through io_uring (cold plans). */
+#define HL_IO_USED_URING (1u << 5)
+
 /* Mirrors transfer.PlanStats (ref transfer.py:167-188) plus the I/O mode actually used. */
 typedef struct hl_plan_stats {
   uint64_t bytes;           /* file bytes moved to HBM                        */
@@ -124,7 +127,7 @@ typedef struct hl_plan_stats {
   uint64_t cufile_bytes;    /* bytes read by cuFile                           */
   uint64_t mmap_bytes;      /* bytes DMA'd from pinned page-cache pages        */
   double ring_setup_seconds;/* pinned ring allocation charged to this call    */
-  uint32_t io_mode_used;    /* bitmask of 1<<hl_io_mode actually used         */
+  uint32_t io_mode_used;    /* bitmask of 1<<hl_io_mode actually used, | HL_IO_USED_URING */
   int32_t numa_node;        /* node the workers and the ring are pinned to (-1: none) */
   double read_seconds;      /* sum over workers: time inside pread / cuFileRead / pinning */
   double wait_seconds;      /* sum over workers: time waiting for a ring slot's DMA      */

@@ -23,7 +23,8 @@ from .errors import NativeUnavailable, raise_native
 LIB_PATH = Path(__file__).resolve().parent / "libhbmload.so"
 
 HL_IO_AUTO, HL_IO_BUFFERED, HL_IO_DIRECT, HL_IO_CUFILE, HL_IO_MMAP = 0, 1, 2, 3, 4
-IO_MODE_NAMES = {HL_IO_BUFFERED: "buffered", HL_IO_DIRECT: "direct", HL_IO_CUFILE: "cufile", HL_IO_MMAP: "mmap"}
+IO_MODE_NAMES = {HL_IO_BUFFERED: "buffered", HL_IO_DIRECT: "direct", HL_IO_CUFILE: "cufile", HL_IO_MMAP: "mmap",
+                 5: "io_uring"}  # 5: HL_IO_USED_URING (hbmload.h)
 IO_MODES = {"auto": HL_IO_AUTO, "buffered": HL_IO_BUFFERED, "direct": HL_IO_DIRECT, "cufile": HL_IO_CUFILE,
             "mmap": HL_IO_MMAP}
 

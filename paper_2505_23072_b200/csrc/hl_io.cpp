@@ -28,11 +28,13 @@
 #include <stdlib.h>
 #include <errno.h>
 #include <fcntl.h>
+#include <linux/io_uring.h>
 #include <pthread.h>
 #include <sched.h>
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
 #include <sys/uio.h>
 #include <unistd.h>
 
@@ -242,6 +244,8 @@ struct PlanRun {
   hl_ctx* ctx;
   cudaEvent_t order_ev = nullptr;  // every H2D waits for it (caller's stream position)
   bool async_tail = false;         // hand the copies' completion to `after` instead of draining
+  uint32_t uring = 0;              // >0: cold plan read by this many io_uring threads (uring_loop)
+  uint32_t uring_depth = 16;       // O_DIRECT reads in flight per io_uring thread
   cudaStream_t after = nullptr;
   const std::vector<Chunk>* chunks;
   std::vector<FileState>* files;
@@ -250,7 +254,7 @@ struct PlanRun {
   std::mutex err_mu;
   int err_code = HL_OK;
   std::string err_msg;
-  std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0}, mmap_bytes{0};
+  std::atomic<uint64_t> direct_bytes{0}, buffered_bytes{0}, cufile_bytes{0}, mmap_bytes{0}, uring_bytes{0};
   double ring_setup = 0;
   std::mutex setup_mu;
   std::atomic<uint64_t> read_ns{0}, wait_ns{0}, submit_ns{0};
@@ -373,6 +377,17 @@ int ensure_slot(hl_ctx* ctx, uint32_t w, uint32_t k, Slot& s) {
 }
 
 static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring);
+static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home);
+
+// The slots a thread of `run` uses: its own ring's, or with io_uring every
+// ring w = u, u + U, u + 2U, ... of the cold team (one read in flight per slot).
+template <class F>
+static void for_each_slot(PlanRun* run, uint32_t w, F&& fn) {
+  hl_ctx* ctx = run->ctx;
+  const uint32_t step = run->uring ? run->uring : ctx->cold_workers + 1;
+  for (uint32_t r = w; r < ctx->cold_workers; r += step)
+    for (auto& s : ctx->rings[r].slots) fn(s);
+}
 
 void worker_main(PlanRun* run, uint32_t w) {
   hl_ctx* ctx = run->ctx;
@@ -400,9 +415,13 @@ void worker_main(PlanRun* run, uint32_t w) {
       return;
     }
   }
-  worker_loop(run, w, ring);
+  if (run->uring) {
+    uring_loop(run, w, ring);
+  } else {
+    worker_loop(run, w, ring);
+  }
   bool pinned = false;  // page-cache ranges pinned for in-flight copies are unpinned only after them
-  for (const auto& s : ring.slots) pinned |= s.reg != nullptr;
+  for_each_slot(run, w, [&](Slot& s) { pinned |= s.reg != nullptr; });
   if (run->async_tail && !pinned && !run->failed.load()) {
     // Completion goes to the caller's stream: it waits for this worker's last
     // copy, so every kernel enqueued there afterwards sees the bytes, and the
@@ -417,13 +436,13 @@ void worker_main(PlanRun* run, uint32_t w) {
   // destination buffers as soon as hl_execute_plan returns, so no DMA of this
   // worker may still be in flight, and no page-cache range may stay pinned.
   cudaError_t e = cudaStreamSynchronize(ring.stream);
-  for (auto& s : ring.slots) {
+  for_each_slot(run, w, [&](Slot& s) {
     s.busy = false;
     if (s.reg) {
       cudaHostUnregister(s.reg);
       s.reg = nullptr;
     }
-  }
+  });
   if (e != cudaSuccess) run->fail(HL_ECUDA, std::string("H2D stream: ") + cudaGetErrorString(e));
 }
 
@@ -586,6 +605,264 @@ static void worker_loop(PlanRun* run, uint32_t w, WorkerRing& ring) {
     s.busy = true;
     run->note_h2d();
   }
+}
+
+// ------------------------------------------------------------------ io_uring cold reader
+// A cold plan is storage-latency bound: its rate follows the O_DIRECT requests
+// in flight. Instead of 32 threads each blocked in one pread, a few threads each
+// keep `uring_depth` reads in flight on an io_uring (raw syscalls, no liburing)
+// and hand every completed read to the H2D stream. Same chunks, same slots,
+// same bytes as worker_loop; io_uring unavailable (kernel, seccomp) or any
+// setup failure falls back to worker_loop.
+struct Uring {
+  int fd = -1;
+  uint8_t *sq = nullptr, *cq = nullptr;
+  size_t sq_sz = 0, cq_sz = 0, sqe_sz = 0;
+  io_uring_sqe* sqes = nullptr;
+  io_uring_cqe* cqes = nullptr;
+  unsigned *sq_tail = nullptr, *sq_mask = nullptr, *sq_array = nullptr;
+  unsigned *cq_head = nullptr, *cq_tail = nullptr, *cq_mask = nullptr;
+
+  bool open(unsigned entries) {
+    io_uring_params p;
+    memset(&p, 0, sizeof p);
+    fd = (int)syscall(__NR_io_uring_setup, entries, &p);
+    if (fd < 0) return false;
+    sq_sz = p.sq_off.array + p.sq_entries * sizeof(unsigned);
+    cq_sz = p.cq_off.cqes + p.cq_entries * sizeof(io_uring_cqe);
+    sqe_sz = p.sq_entries * sizeof(io_uring_sqe);
+    void* a = mmap(nullptr, sq_sz, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, IORING_OFF_SQ_RING);
+    void* b = mmap(nullptr, cq_sz, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, IORING_OFF_CQ_RING);
+    void* c = mmap(nullptr, sqe_sz, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, IORING_OFF_SQES);
+    sq = a == MAP_FAILED ? nullptr : (uint8_t*)a;
+    cq = b == MAP_FAILED ? nullptr : (uint8_t*)b;
+    sqes = c == MAP_FAILED ? nullptr : (io_uring_sqe*)c;
+    if (!sq || !cq || !sqes) return false;
+    sq_tail = (unsigned*)(sq + p.sq_off.tail);
+    sq_mask = (unsigned*)(sq + p.sq_off.ring_mask);
+    sq_array = (unsigned*)(sq + p.sq_off.array);
+    cq_head = (unsigned*)(cq + p.cq_off.head);
+    cq_tail = (unsigned*)(cq + p.cq_off.tail);
+    cq_mask = (unsigned*)(cq + p.cq_off.ring_mask);
+    cqes = (io_uring_cqe*)(cq + p.cq_off.cqes);
+    return true;
+  }
+  ~Uring() {
+    if (sqes) munmap(sqes, sqe_sz);
+    if (cq) munmap(cq, cq_sz);
+    if (sq) munmap(sq, sq_sz);
+    if (fd >= 0) ::close(fd);
+  }
+  void read(int file, void* buf, uint32_t len, uint64_t off, uint64_t tag) {
+    const unsigned tail = *sq_tail;
+    const unsigned idx = tail & *sq_mask;
+    io_uring_sqe* e = &sqes[idx];
+    memset(e, 0, sizeof *e);
+    e->opcode = IORING_OP_READ;
+    e->fd = file;
+    e->addr = (uint64_t)(uintptr_t)buf;
+    e->len = len;
+    e->off = off;
+    e->user_data = tag;
+    sq_array[idx] = idx;
+    __atomic_store_n(sq_tail, tail + 1, __ATOMIC_RELEASE);
+  }
+  // submit `n` queued reads, wait for at least `wait` completions
+  int enter(unsigned n, unsigned wait) {
+    for (;;) {
+      int r = (int)syscall(__NR_io_uring_enter, fd, n, wait, wait ? IORING_ENTER_GETEVENTS : 0, nullptr, 0);
+      if (r >= 0 || errno != EINTR) return r < 0 ? -errno : r;
+    }
+  }
+  template <class F>
+  void reap(F&& fn) {
+    unsigned head = *cq_head;
+    while (head != __atomic_load_n(cq_tail, __ATOMIC_ACQUIRE)) {
+      const io_uring_cqe& c = cqes[head & *cq_mask];
+      fn(c.user_data, c.res);
+      ++head;
+    }
+    __atomic_store_n(cq_head, head, __ATOMIC_RELEASE);
+  }
+};
+
+static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
+  hl_ctx* ctx = run->ctx;
+  const auto& chunks = *run->chunks;
+  auto& files = *run->files;
+  // this thread's slots: every slot of rings u, u + U, ... (streams/events made on first use)
+  std::vector<Slot*> slots;
+  for (uint32_t r = u; r < ctx->cold_workers; r += run->uring) {
+    WorkerRing& wr = ctx->rings[r];
+    int rc = ensure_ring(ctx, wr);
+    for (uint32_t k = 0; rc == HL_OK && k < wr.slots.size(); ++k) {
+      rc = ensure_slot(ctx, r, k, wr.slots[k]);
+      slots.push_back(&wr.slots[k]);
+    }
+    if (rc) {
+      run->fail(rc, hl_last_error());
+      return;
+    }
+  }
+  const uint32_t depth = (uint32_t)std::min<size_t>(run->uring_depth, slots.size());
+  Uring ring;
+  if (depth == 0 || !ring.open(depth)) {
+    worker_loop(run, u, home);  // no io_uring here: the same chunks with blocking reads
+    return;
+  }
+  struct Req {
+    const Chunk* c = nullptr;
+    uint64_t aoff = 0, alen = 0;
+    bool reading = false;
+  };
+  std::vector<Req> req(slots.size());
+  std::vector<unsigned char> vec;  // mincore scratch
+  size_t hint = 0;
+  uint32_t inflight = 0;
+  bool claiming = true;
+  auto h2d = [&](Slot& s, const Chunk& c, uint64_t head) -> bool {
+    const double ts = now_s();
+    cudaError_t e = cudaMemcpyAsync((void*)c.dst, s.host + head, c.len, cudaMemcpyHostToDevice, home.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(s.ev, home.stream);
+    run->submit_ns += (uint64_t)((now_s() - ts) * 1e9);
+    if (e != cudaSuccess) {
+      run->fail(HL_ECUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
+      return false;
+    }
+    s.busy = true;
+    run->note_h2d();
+    return true;
+  };
+  // a slot with no read in flight whose previous DMA (if any) is done; -1 if none
+  auto free_slot = [&](bool block) -> long {
+    for (size_t n = 0; n < slots.size(); ++n) {
+      const size_t i = (hint + n) % slots.size();
+      Slot& s = *slots[i];
+      if (req[i].reading) continue;
+      if (s.busy) {
+        if (cudaEventQuery(s.ev) != cudaSuccess) continue;
+        s.busy = false;
+      }
+      hint = i + 1;
+      return (long)i;
+    }
+    if (!block) return -1;
+    for (size_t n = 0; n < slots.size(); ++n) {  // every slot is DMA-busy: wait for the next in order
+      const size_t i = (hint + n) % slots.size();
+      if (req[i].reading) continue;
+      const double tw = now_s();
+      cudaError_t e = cudaEventSynchronize(slots[i]->ev);
+      run->wait_ns += (uint64_t)((now_s() - tw) * 1e9);
+      if (e != cudaSuccess) {
+        run->fail(HL_ECUDA, std::string("H2D completion: ") + cudaGetErrorString(e));
+        return -1;
+      }
+      slots[i]->busy = false;
+      hint = i + 1;
+      return (long)i;
+    }
+    return -1;
+  };
+  while (!run->failed.load(std::memory_order_relaxed)) {
+    unsigned queued = 0;
+    while (claiming && inflight < depth) {
+      const long si = free_slot(inflight == 0);
+      if (si < 0) break;  // wait for completions first
+      const size_t i = run->cursor.fetch_add(1);
+      if (i >= chunks.size()) {
+        claiming = false;
+        break;
+      }
+      const Chunk& c = chunks[i];
+      FileState& f = files[c.file];
+      Slot& s = *slots[si];
+      const uint64_t head = c.off % kAlign;
+      bool direct = f.dfd >= 0 && (f.mode == HL_IO_AUTO || f.mode == HL_IO_DIRECT);
+      if (direct && f.mode == HL_IO_AUTO && f.probe) {
+        // a chunk already in the page cache is copied from it (no storage read)
+        const uint64_t p0 = c.off / kAlign, p1 = (c.off + c.len + kAlign - 1) / kAlign;
+        if (vec.size() < p1 - p0) vec.resize(p1 - p0);
+        bool resident = mincore(f.probe + p0 * kAlign, (p1 - p0) * kAlign, vec.data()) == 0;
+        for (uint64_t q = 0; resident && q < p1 - p0; ++q) resident = vec[q] & 1;
+        direct = !resident;
+      }
+      if (!direct) {
+        uint64_t got = 0;
+        int err = 0;
+        const double tr = now_s();
+        if (!pread_full(f.bfd, s.host + head, c.len, c.off, &got, &err) || got < c.len) {
+          run->fail(HL_EIO, err ? std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err)
+                                : "unexpected EOF at file offset " + std::to_string(c.off + got));
+          return;
+        }
+        run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
+        run->buffered_bytes += c.len;
+        if (!h2d(s, c, head)) return;
+        continue;
+      }
+      Req& q = req[si];
+      q.c = &c;
+      q.aoff = round_down(c.off, kAlign);
+      q.alen = round_up(c.off + c.len, kAlign) - q.aoff;
+      q.reading = true;
+      ring.read(f.dfd, s.host, (uint32_t)q.alen, q.aoff, (uint64_t)si);
+      ++queued;
+      ++inflight;
+    }
+    if (!claiming && inflight == 0) break;
+    const double tr = now_s();
+    const int r = ring.enter(queued, inflight ? 1 : 0);
+    run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
+    if (r < 0) {
+      run->fail(HL_EIO, std::string("io_uring_enter: ") + strerror(-r));
+      return;
+    }
+    bool ok = true;
+    ring.reap([&](uint64_t tag, int res) {
+      Req& q = req[tag];
+      Slot& s = *slots[tag];
+      const Chunk& c = *q.c;
+      FileState& f = files[c.file];
+      q.reading = false;
+      --inflight;
+      if (!ok) return;
+      const uint64_t head = c.off % kAlign;
+      const uint64_t need = c.off + c.len - q.aoff;  // bytes the chunk needs from the aligned start
+      uint64_t got = res > 0 ? (uint64_t)res : 0;
+      int err = res < 0 ? -res : 0;
+      if (res == -EINVAL) {  // no O_DIRECT on this file system: buffered
+        err = 0;
+        uint64_t n = 0;
+        if (!pread_full(f.bfd, s.host + head, c.len, c.off, &n, &err) || n < c.len) {
+          ok = false;
+          run->fail(HL_EIO, "read failed at offset " + std::to_string(c.off));
+          return;
+        }
+        run->buffered_bytes += c.len;
+        ok = h2d(s, c, head);
+        return;
+      }
+      if (!err && got < need && got % kAlign == 0) {  // short read: finish it synchronously
+        uint64_t n = 0;
+        if (pread_full(f.dfd, s.host + got, q.alen - got, q.aoff + got, &n, &err)) got += n;
+      }
+      if (err || got < need) {
+        ok = false;
+        run->fail(HL_EIO, err ? std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err)
+                              : "unexpected EOF at file offset " + std::to_string(q.aoff + got));
+        return;
+      }
+      run->direct_bytes += c.len;
+      run->uring_bytes += c.len;
+      ok = h2d(s, c, head);
+    });
+    if (!ok) break;
+  }
+  // a failure can leave reads in flight into our slots: let them land before the slots are reused
+  while (inflight > 0 && ring.enter(0, 1) >= 0) ring.reap([&](uint64_t tag, int) {
+      req[tag].reading = false;
+      --inflight;
+    });
 }
 
 void team_thread(hl_ctx* ctx, uint32_t w) {
@@ -915,10 +1192,26 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
       o += n;
     }
   }
-  const uint32_t nw = (uint32_t)std::min<size_t>(team, std::max<size_t>(chunks.size(), 1));
+  uint32_t nw = (uint32_t)std::min<size_t>(team, std::max<size_t>(chunks.size(), 1));
+  uint32_t ring_workers = nw;
+  // Cold plans on io_uring (default; $HL_COLD_URING=0 keeps the blocking readers):
+  // $HL_URING_THREADS threads x $HL_URING_DEPTH reads in flight, using the slots
+  // of the whole cold team. cuFile / mmap plans keep their own paths.
+  const char* ue = getenv("HL_COLD_URING");
+  if (cold_plan && !(ue && ue[0] == '0') && !(mode_mask & ((1u << HL_IO_CUFILE) | (1u << HL_IO_MMAP)))) {
+    auto env_u32 = [](const char* name, long dflt, long lo, long hi) {
+      const char* v = getenv(name);
+      return (uint32_t)std::max(lo, std::min(v ? strtol(v, nullptr, 10) : dflt, hi));
+    };
+    run.uring = std::min(env_u32("HL_URING_THREADS", 2, 1, 16), ctx->cold_workers);
+    run.uring_depth = env_u32("HL_URING_DEPTH", 16, 1, 256);
+    nw = (uint32_t)std::min<size_t>(run.uring, std::max<size_t>(chunks.size(), 1));
+    run.uring = nw;
+    ring_workers = ctx->cold_workers;
+  }
   {
     double secs = 0;
-    int rc = ensure_ring_memory(ctx, nw, &secs);
+    int rc = ensure_ring_memory(ctx, ring_workers, &secs);
     if (rc) {
       close_all();
       return rc;
@@ -942,7 +1235,8 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     stats->io_mode_used = (run.buffered_bytes.load() ? 1u << HL_IO_BUFFERED : 0u) |
                           (run.direct_bytes.load() ? 1u << HL_IO_DIRECT : 0u) |
                           (run.cufile_bytes.load() ? 1u << HL_IO_CUFILE : 0u) |
-                          (run.mmap_bytes.load() ? 1u << HL_IO_MMAP : 0u);
+                          (run.mmap_bytes.load() ? 1u << HL_IO_MMAP : 0u) |
+                          (run.uring_bytes.load() ? HL_IO_USED_URING : 0u);
     stats->numa_node = ctx->cfg.numa_node;
     stats->read_seconds = run.read_ns.load() * 1e-9;
     stats->wait_seconds = run.wait_ns.load() * 1e-9;

@@ -122,7 +122,7 @@ def test_c2_llama7b_full_get_tensor():
     loader = SafeTensorsFileLoader(SingleGroup(), "host")
     loader.add_filenames({0: paths})
     fb = loader.copy_files_to_device()
-    assert set(loader.last_transfer_stats.io_modes) <= {"buffered", "direct", "mmap"}
+    assert set(loader.last_transfer_stats.io_modes) <= {"buffered", "direct", "mmap", "io_uring"}
     for k in [e[0] for e in synth.entries("llama2-7b")]:
         v = fb.get_tensor(k)
         assert np.array_equal(_host(v), expect[k][2]), k

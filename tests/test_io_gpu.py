@@ -213,8 +213,51 @@ def test_cold_plans_run_on_the_cold_team(blob):
     _native.drop_cache(str(path))
     dst.zero_()
     cold = eng.execute([str(path)], [(0, 0, 0, n, dst.data_ptr())], after_stream=0)
-    assert cold["workers"] > 4 and "direct" in cold["io_modes"], cold
+    # io_uring threads with many reads in flight, or (io_uring unavailable) the larger team
+    assert "direct" in cold["io_modes"], cold
+    assert "io_uring" in cold["io_modes"] or cold["workers"] > 4, cold
     assert np.array_equal(dst.cpu().numpy(), data[:n])
+    eng.close()
+
+
+@pytest.mark.parametrize("uring", ["1", "0"])
+def test_cold_reader_paths_give_identical_bytes(blob, monkeypatch, uring):
+    """Cold plans read through io_uring (HL_COLD_URING, default on) or the
+    blocking reader team (HL_COLD_URING=0): ragged ranges at odd offsets,
+    the file's last bytes (a short O_DIRECT read at EOF), a partly resident
+    file, tiny rings (reads wait on slot DMAs), and the async tail — the same
+    bytes either way."""
+    monkeypatch.setenv("HL_COLD_URING", uring)
+    monkeypatch.setenv("HL_URING_DEPTH", "5")
+    path, data = blob
+    rng = np.random.default_rng(11)
+    ranges = [(0, 3 << 20), (13281, (5 << 20) + 7), (data.size - 9, 9), (4095, 2)]
+    for _ in range(8):
+        off = int(rng.integers(0, data.size - 1))
+        ranges.append((off, int(rng.integers(1, min(7 << 20, data.size - off)))))
+    total = sum(n for _, n in ranges)
+    s = torch.cuda.current_stream().cuda_stream
+    eng = _native.IoEngine(0, workers=3, chunk_bytes=1 << 20, slots_per_worker=2, io_mode="auto")
+    for resident in (False, True, "half"):
+        _native.drop_cache(str(path))
+        if resident is True:
+            path.read_bytes()
+        elif resident == "half":
+            with open(path, "rb") as f:
+                f.read(data.size // 2)
+        dst = torch.zeros(total + 64, dtype=torch.uint8, device="cuda")
+        blocks, cur = [], 0
+        for i, (off, n) in enumerate(ranges):
+            blocks.append((0, i, off, n, dst.data_ptr() + cur))
+            cur += n
+        st = eng.execute([str(path)], blocks, after_stream=s, async_tail=True)
+        got = dst.cpu().numpy()  # after the stream: the copies' completion was handed to it
+        cur = 0
+        for off, n in ranges:
+            assert np.array_equal(got[cur:cur + n], data[off:off + n]), (uring, resident, off, n)
+            cur += n
+        if resident is False:
+            assert ("io_uring" in st["io_modes"]) == (uring == "1"), st
     eng.close()
 
 

@@ -359,3 +359,27 @@ def test_planes_replay_reference_op_traces(plane):
         for rank_result in _run(world, fn, timeout=600):
             bad = {k: v for k, v in rank_result.items() if v is not True}
             assert rank_result and not bad, (world, bad)
+
+
+def fanout_job(rank, world):
+    """The peer-memory plane's broadcast route (loader._fanout_route): at
+    W >= 3 replicated tensors over BIG_BROADCAST go through the broadcast
+    instead of W-1 peer pulls. BIG_BROADCAST = 0 sends every replicated
+    tensor that way: golden corpora key by key and batched, and every
+    reference op trace (repeated / stale / survivor keys)."""
+    from paper_2505_23072_b200 import loader
+
+    loader.BIG_BROADCAST = 0
+    out = {("keys",) + k: v for k, v in golden_job(rank, world, plane="ipc").items()}
+    out.update({("batch",) + k: v for k, v in golden_job(rank, world, plane="ipc", batched=True).items()})
+    out.update({("ops", k): v for k, v in ops_job(rank, world, "ipc").items()})
+    out.update({("ops_batched", k): v for k, v in ops_job(rank, world, "ipc", batched=True).items()})
+    return out
+
+
+@pytest.mark.parametrize("world", [3, 4])
+@pytest.mark.timeout(900)
+def test_ipc_plane_fanout_route_matches_reference(world):
+    for rank_result in _run(world, fanout_job, timeout=800):
+        bad = {k: v for k, v in rank_result.items() if v is not True}
+        assert rank_result and not bad, (world, bad)
