@@ -246,6 +246,7 @@ struct PlanRun {
   bool async_tail = false;         // hand the copies' completion to `after` instead of draining
   uint32_t uring = 0;              // >0: cold plan read by this many io_uring threads (uring_loop)
   uint32_t uring_depth = 16;       // O_DIRECT reads in flight per io_uring thread
+  uint32_t uring_rings = 0;        // io_uring threads share the slots of rings [0, uring_rings)
   cudaStream_t after = nullptr;
   const std::vector<Chunk>* chunks;
   std::vector<FileState>* files;
@@ -384,8 +385,9 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home);
 template <class F>
 static void for_each_slot(PlanRun* run, uint32_t w, F&& fn) {
   hl_ctx* ctx = run->ctx;
-  const uint32_t step = run->uring ? run->uring : ctx->cold_workers + 1;
-  for (uint32_t r = w; r < ctx->cold_workers; r += step)
+  const uint32_t end = run->uring ? run->uring_rings : ctx->cold_workers;
+  const uint32_t step = run->uring ? run->uring : end + 1;
+  for (uint32_t r = w; r < end; r += step)
     for (auto& s : ctx->rings[r].slots) fn(s);
 }
 
@@ -692,7 +694,7 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
   auto& files = *run->files;
   // this thread's slots: every slot of rings u, u + U, ... (streams/events made on first use)
   std::vector<Slot*> slots;
-  for (uint32_t r = u; r < ctx->cold_workers; r += run->uring) {
+  for (uint32_t r = u; r < run->uring_rings; r += run->uring) {
     WorkerRing& wr = ctx->rings[r];
     int rc = ensure_ring(ctx, wr);
     for (uint32_t k = 0; rc == HL_OK && k < wr.slots.size(); ++k) {
@@ -1207,7 +1209,12 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     run.uring_depth = env_u32("HL_URING_DEPTH", 16, 1, 256);
     nw = (uint32_t)std::min<size_t>(run.uring, std::max<size_t>(chunks.size(), 1));
     run.uring = nw;
-    ring_workers = ctx->cold_workers;
+    // enough slots for every read in flight plus a few DMAs behind them: the warm team's
+    // rings, grown if need be (not the whole 32-worker cold team's 384 MiB)
+    const uint32_t spw = ctx->cfg.slots_per_worker;
+    const uint32_t want = (nw * (run.uring_depth + 4) + spw - 1) / spw;
+    ring_workers = std::min(ctx->cold_workers, std::max(std::max(ctx->cfg.workers, want), nw));
+    run.uring_rings = ring_workers;
   }
   {
     double secs = 0;
