@@ -39,6 +39,8 @@ from .format import DType, TensorMetadata
 __all__ = ["ProcessGroup", "SingleGroup", "DistGroup", "ShardSpec", "partition"]
 
 DEFAULT_TIMEOUT = 30.0
+_BARRIER_SEQ: dict[tuple[str, str], int] = {}  # DistGroup.bounded_barrier calls so far, per member set
+_BARRIER_LOCK = threading.Lock()
 
 
 @dataclass(frozen=True)
@@ -441,9 +443,12 @@ class DistGroup:
         from torch.distributed import distributed_c10d as c10d
 
         store = c10d._get_default_store()
-        self._barrier_seq = getattr(self, "_barrier_seq", 0) + 1
         members = "all" if self.pg is None else ",".join(map(str, c10d.get_process_group_ranks(self.pg)))
-        key = f"hl-barrier/{members}/{tag}/{self._barrier_seq}"
+        # the sequence number is per process and member set, not per DistGroup object: a later
+        # group over the same ranks must not meet at keys an earlier one already filled
+        with _BARRIER_LOCK:
+            seq = _BARRIER_SEQ[(members, tag)] = _BARRIER_SEQ.get((members, tag), 0) + 1
+        key = f"hl-barrier/{members}/{tag}/{seq}"
         limit = self.timeout if timeout is None else timeout
         deadline = time.monotonic() + limit
         arrived = store.add(key, 1)

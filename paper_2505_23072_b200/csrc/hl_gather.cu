@@ -891,6 +891,8 @@ struct alignas(64) TileDesc {
   int32_t c0;           // first source column of the segment (tensor-map elements)
   uint32_t bx, by;      // box dims (elements, rows)
   uint32_t in_bytes;    // bytes of one source box (mbarrier transaction count)
+  uint16_t grp;         // descriptors in this one's interleave group (>= 1, see tile_unit)
+  uint16_t gi;          // index in the group
 };
 static_assert(sizeof(TileDesc) == 320, "TileDesc layout");
 
@@ -906,10 +908,22 @@ struct TileUnit {
   int32_t sx, sy, dx;  // source box origin (col, row), destination col (row = sy)
 };
 
+// Descriptors come in interleave groups: `grp` consecutive descriptors with the
+// same unit count share one unit range, unit u of the group being unit u / grp
+// of member u % grp. The W shards of one tensor form a group, so the boxes the
+// grid streams at any moment are the same rows of every shard — whole source
+// rows — instead of one narrow column band at the source pitch (which leaves
+// HBM channels idle). `di` always names a group's first member.
 __device__ __forceinline__ TileUnit tile_unit(const TileParams& p, uint64_t u, uint32_t& di) {
-  while (di + 1 < p.n && p.d[di + 1].unit_begin <= u) ++di;
-  const TileDesc& d = p.d[di];
-  const uint64_t lu = u - d.unit_begin;
+  for (;;) {
+    const uint32_t nx = di + p.d[di].grp;
+    if (nx < p.n && p.d[nx].unit_begin <= u) di = nx;
+    else break;
+  }
+  const uint64_t lg = u - p.d[di].unit_begin;
+  const uint32_t g = p.d[di].grp;
+  const TileDesc& d = p.d[di + (uint32_t)(lg % g)];
+  const uint64_t lu = lg / g;
   const uint32_t by = (uint32_t)(lu / d.nbx), bx = (uint32_t)(lu % d.nbx);
   TileUnit t;
   t.d = &d;
@@ -1227,6 +1241,16 @@ static EncodeTiled encode_tiled() {
   return fn;
 }
 
+// Largest interleave group (tile_unit); $HL_TILE_GROUP=1 keeps descriptor-major order.
+static size_t tile_group() {
+  static const size_t g = [] {
+    const char* e = getenv("HL_TILE_GROUP");
+    const long v = e ? strtol(e, nullptr, 10) : 16;
+    return (size_t)std::max(1L, std::min(v, 64L));
+  }();
+  return g;
+}
+
 static bool tiles_enabled() {
   static const bool on = [] {
     const char* e = getenv("HL_GATHER_TILES");
@@ -1467,14 +1491,26 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
     if (!tp) tp = new TileParams();
     tp->n = 0;
     tp->total_units = 0;
-    for (size_t i = 0; i < tiles[kind].size(); ++i) {
-      tiles[kind][i].unit_begin = tp->total_units;
-      tp->d[tp->n++] = tiles[kind][i];
-      tp->total_units += tile_units[kind][i];
-      if (tp->n == (uint32_t)kMaxTiles) {
+    const auto& tv = tiles[kind];
+    const auto& uv = tile_units[kind];
+    for (size_t i = 0; i < tv.size();) {
+      // an interleave group: consecutive tiles with equal unit counts (a tensor's W shards)
+      size_t j = i + 1;
+      while (j < tv.size() && j - i < tile_group() && uv[j] == uv[i]) ++j;
+      const uint32_t g = (uint32_t)(j - i);
+      if (tp->n + g > (uint32_t)kMaxTiles) {
         int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
         if (rc) return rc;
       }
+      for (uint32_t m = 0; m < g; ++m) {
+        TileDesc& t = tp->d[tp->n++];
+        t = tv[i + m];
+        t.unit_begin = tp->total_units;
+        t.grp = (uint16_t)g;
+        t.gi = (uint16_t)m;
+      }
+      tp->total_units += (uint64_t)g * uv[i];
+      i = j;
     }
     int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
     if (rc) return rc;

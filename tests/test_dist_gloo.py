@@ -81,6 +81,16 @@ def _worker(rank, world, port, q):
         # passes when everyone arrives, raises instead of hanging when a rank never does
         g.bounded_barrier("both", timeout=30)
         out["bounded"] = True
+        # a later group over the same ranks meets at fresh keys (its first barrier must
+        # still wait for the late rank, not pass on the earlier group's filled counter)
+        import time
+
+        g2 = DistGroup(check_order=False)
+        if rank == 1:
+            time.sleep(1.0)
+        t0 = time.monotonic()
+        g2.bounded_barrier("both", timeout=30)
+        out["second_group_waited"] = rank == 1 or time.monotonic() - t0 > 0.7
         out["alone"] = True
         if rank == 0:
             try:
@@ -112,6 +122,7 @@ def test_distgroup_two_ranks_gloo():
         assert res[r]["mismatch"] is True
         assert res[r]["bcast"] == list(range(10))
         assert res[r]["bounded"] is True and res[r]["alone"] is True
+        assert res[r]["second_group_waited"] is True
     raw = res[0]["raw"]
     full = np.frombuffer(raw, dtype=np.int16).reshape(7, 5)
     for dim in (0, 1):

@@ -317,3 +317,31 @@ def test_many_column_shards_span_tile_launches():
         cd = (cd + rows * seg * SIZES[ddt] + 15) & ~15
     got, exp = run_both(src, cd, descs)
     assert_same(got, exp)
+
+
+@pytest.mark.parametrize("world", [7, 8])
+def test_interleaved_shard_groups_across_launches(world):
+    """A tensor's W column shards form one interleave group (tile_unit: unit u
+    of the group is unit u / W of shard u % W), so the grid streams the same
+    rows of every shard together. 40 tensors x W shards is more than one tile
+    launch carries (96): groups never straddle a launch (W=7 leaves a gap);
+    uneven splits give shards of different widths (partial groups); casts and
+    raw copies mixed. Against the oracle, with sentinels."""
+    rng = np.random.default_rng(500 + world)
+    src = rng.integers(0, 256, size=48 << 20, dtype=np.uint8)
+    descs, cs, cd = [], 0, 0
+    for i in range(40):
+        rows = int(rng.choice([16, 40, 300]))
+        cols = 8 * world * int(rng.integers(4, 40)) + (8 * int(rng.integers(0, world)) if i % 4 == 3 else 0)
+        sdt, ddt = [(10, 10), (10, 9), (11, 9), (1, 1)][i % 4]
+        ss = SIZES[sdt]
+        if cs + rows * cols * ss + 64 > src.size:
+            break
+        for r in range(world):
+            lo, hi = kernels.shard_bounds(cols, world, r)
+            descs.append((cs + lo * ss, cd, rows, hi - lo, cols * ss, sdt, ddt))
+            cd = (cd + rows * (hi - lo) * SIZES[ddt] + 15) & ~15
+        cs = (cs + rows * cols * ss + 15) & ~15
+    assert len(descs) > 96
+    got, exp = run_both(src, cd, descs)
+    assert_same(got, exp)
