@@ -1169,6 +1169,16 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
     if (cold_bytes * 2 > (double)total) team = ctx->cold_workers;
   }
   const bool cold_plan = team > ctx->cfg.workers;
+  // Small warm plans (< 2 GiB) on a large team (>= 8) run on half of it: their copy engine,
+  // not the page-cache copies, is the bound, and fewer concurrent copies leave it more
+  // host-memory bandwidth (GPT-2's 0.5 GB from a warm cache: 6 workers 12.2-12.4 ms to ready,
+  // 12 workers 13.3-13.5, 16 workers 14.1; profiles/r02_c1_timeline.txt, r02_ring_sweep.jsonl).
+  // Small teams (an explicit worker cap) are kept. $HL_SMALL_TEAM overrides.
+  if (!cold_plan && total < (2ull << 30)) {
+    const char* e = getenv("HL_SMALL_TEAM");
+    const long v = e ? strtol(e, nullptr, 10) : (team >= 8 ? (long)(team + 1) / 2 : (long)team);
+    team = (uint32_t)std::max(1L, std::min(v, (long)team));
+  }
   // Chunk size. Plans under 2 GiB are cut into 2 MiB chunks: the pipeline fill
   // (first reads before any DMA) and drain are a visible part of a sub-second
   // load (GPT-2's 0.5 GB: 10.6 vs 11.3 ms engine at 4 MiB;

@@ -281,3 +281,21 @@ def test_async_plans_hand_completion_to_the_stream(blob):
     for off, got in outs:
         assert np.array_equal(got.cpu().numpy(), data[off:off + n]), off
     eng.close()
+
+
+def test_small_warm_plans_run_on_half_a_large_team(blob, monkeypatch):
+    """A warm plan under 2 GiB on a team of >= 8 runs on half of it (its copy
+    engine is the bound; fewer concurrent page-cache copies leave it more host
+    memory bandwidth); $HL_SMALL_TEAM overrides; bytes exact either way."""
+    path, data = blob
+    n = 24 << 20
+    path.read_bytes()
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+    eng = _native.IoEngine(0, workers=8, chunk_bytes=1 << 20, io_mode="auto")
+    st = eng.execute([str(path)], [(0, 0, 0, n, dst.data_ptr())], after_stream=0)
+    assert st["workers"] == 4 and np.array_equal(dst.cpu().numpy(), data[:n]), st
+    monkeypatch.setenv("HL_SMALL_TEAM", "8")
+    dst.zero_()
+    st = eng.execute([str(path)], [(0, 0, 0, n, dst.data_ptr())], after_stream=0)
+    assert st["workers"] == 8 and np.array_equal(dst.cpu().numpy(), data[:n]), st
+    eng.close()
