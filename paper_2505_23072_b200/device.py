@@ -68,6 +68,8 @@ GDS_ALIGNMENT = 4096                 # cuFile / O_DIRECT block granularity
 DEFAULT_HOST_BOUNCE = 4 * 1024 * 1024  # pinned chunk per pread + H2D hop (ref: 160 MiB host bounce; 4 MiB measured best, profiles/)
 DEFAULT_ALIGN_BOUNCE = 16 * 1024 * 1024  # kept for API parity; the realign kernel needs no bounce
 CARVE_CHUNK = 1 << 30                # largest shared chunk per-key outputs are carved from
+CARVE_SMALL = 1 << 20                # outputs below this (norms, biases) share their own chunks...
+CARVE_SMALL_CHUNK = 16 << 20         # ...of this size, so keeping one of them pins 16 MiB, not 1 GiB
 
 
 class BackendKind(Enum):
@@ -217,6 +219,8 @@ class DevicePool:
         # carving: per-key outputs sliced from shared chunks (see _carve)
         self._chunk: torch.Tensor | None = None
         self._chunk_off = 0
+        self._small: torch.Tensor | None = None  # chunk for outputs under CARVE_SMALL
+        self._small_off = 0
         self._expect = 0
 
     def expect(self, nbytes: int) -> None:
@@ -229,6 +233,7 @@ class DevicePool:
         """Drop the pool's reference to the current chunk (slices keep theirs)."""
         with self._lock:
             self._chunk, self._chunk_off, self._expect = None, 0, 0
+            self._small, self._small_off = None, 0
 
     def _carve(self, nbytes: int) -> torch.Tensor:
         """A 256-byte aligned slice of a shared chunk. A fresh process pays
@@ -237,9 +242,20 @@ class DevicePool:
         announced remaining bytes, at most CARVE_CHUNK) turns a first load's
         ~1 s of allocator growth into a few calls. Accounting stays per buffer;
         a chunk's memory returns when its last slice dies — so a caller that
-        keeps one small output alive keeps its whole chunk (at most CARVE_CHUNK,
-        and never more than the handle's announced outputs) resident. With a
-        ``capacity_cap`` nothing is carved (``allocate``)."""
+        keeps one output alive keeps its whole chunk resident: at most
+        CARVE_CHUNK (and never more than the handle's announced outputs) for a
+        weight, CARVE_SMALL_CHUNK for an output under CARVE_SMALL (norms and
+        biases are carved apart from the weights). With a ``capacity_cap``
+        nothing is carved (``allocate``)."""
+        if nbytes < CARVE_SMALL:
+            # small outputs get their own chunks: a caller that keeps only a few norms
+            # or biases then pins CARVE_SMALL_CHUNK, not a big chunk of weights
+            if self._small is None or self._small_off + nbytes > self._small.numel():
+                self._small = torch.empty(CARVE_SMALL_CHUNK, dtype=torch.uint8, device=self.device)
+                self._small_off = 0
+            t = self._small[self._small_off:self._small_off + nbytes]
+            self._small_off += (nbytes + 255) & ~255
+            return t
         if self._chunk is None or self._chunk_off + nbytes > self._chunk.numel():
             size = max(nbytes, min(CARVE_CHUNK, max(self._expect, nbytes)))
             self._chunk = torch.empty(size, dtype=torch.uint8, device=self.device)
@@ -273,6 +289,7 @@ class DevicePool:
                         t = self._carve(max(size, 1) + 16)
                     except torch.OutOfMemoryError:
                         self._chunk, self._chunk_off = None, 0
+                        self._small, self._small_off = None, 0
                         t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)
                 else:
                     t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)

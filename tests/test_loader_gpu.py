@@ -566,3 +566,33 @@ def test_deferred_clone_batches(tmp_path, rng):
         assert v.torch.reshape(-1).view(torch.uint8).cpu().numpy().tobytes() == exp, k
     fb.close()
     ld.close()
+
+
+def test_kept_small_outputs_pin_a_small_chunk(tmp_path, rng):
+    """auto_release outputs are carved from shared chunks (one cudaMalloc per
+    chunk, not per key); outputs under CARVE_SMALL (norms, biases) come from
+    their own CARVE_SMALL_CHUNK chunks, so a caller that keeps only those pins
+    16 MiB, not a chunk of weights (ref device.py:191-214 releases per buffer)."""
+    from paper_2505_23072_b200 import device
+
+    t = {"w0": (DType.BF16, (2048, 1024), rng.integers(0, 256, 4 << 20, dtype=np.uint8).tobytes()),
+         "n0": (DType.BF16, (1024,), rng.integers(0, 256, 2048, dtype=np.uint8).tobytes()),
+         "w1": (DType.BF16, (1024, 1024), rng.integers(0, 256, 2 << 20, dtype=np.uint8).tobytes()),
+         "b1": (DType.F32, (1024,), rng.integers(0, 256, 4096, dtype=np.uint8).tobytes())}
+    p = _write(tmp_path, "m.safetensors", t)
+    loader = SafeTensorsFileLoader(SingleGroup(), "host")
+    loader.add_filenames({0: [p]})
+    fb = loader.copy_files_to_device()
+    got = {k: fb.get_tensor(k) for k in t}
+    for k, (_, _, raw) in t.items():
+        assert got[k].tobytes() == raw, k
+    small = {k: got[k].torch.untyped_storage().nbytes() for k in ("n0", "b1")}
+    big = {k: got[k].torch.untyped_storage().nbytes() for k in ("w0", "w1")}
+    assert all(v == device.CARVE_SMALL_CHUNK for v in small.values()), small
+    assert all(v >= (4 << 20) + (2 << 20) for v in big.values()), big  # the weights share one chunk
+    kept = got["n0"].torch
+    del got
+    fb.close()
+    loader.close()
+    assert kept.untyped_storage().nbytes() == device.CARVE_SMALL_CHUNK
+    assert kept.view(torch.uint8).cpu().numpy().tobytes() == t["n0"][2]
