@@ -874,7 +874,8 @@ def main():
                "io_modes": sorted(io_modes), "page_cache_residency_before": resid,
                "first_load_seconds_in_process": round(first_ms / 1e3, 4) if first_ms else None,
                "phases_ms": {k: round(statistics.median(p[k] for p in phases), 2) for k in phases[-1]},
-               "numa": {"node": st.numa_node, "cpus": len(st.numa_cpus), "io_threads": st.io_threads} if st else None}
+               "numa": {"node": st.numa_node, "cpus": len(st.numa_cpus), "io_threads": st.io_threads,
+                        "storage_nodes": sorted(set(st.storage_numa_nodes))} if st else None}
         if world > 1:
             rm = statistics.median(ret_ms)
             link = max(gather_ranks(recv_bytes))

@@ -186,6 +186,12 @@ int hl_ctx_cpus(const hl_ctx* ctx, int32_t* cpus, uint32_t cap, uint32_t* n_cpus
  * Topology / 274-293 worker affinity). */
 int hl_topology_resolve(const char* pci_bus_id, int32_t requested_node, int32_t* node, int32_t* cpus,
                         uint32_t cap, uint32_t* n_cpus);
+/* NUMA node of the storage device holding `path` (the NVMe / virtio / HBA PCI
+ * function that /sys/dev/block/MAJ:MIN resolves to; honours $HL_SYSFS_ROOT),
+ * -1 when unknown (tmpfs, overlay). Reported beside the engine's node: the ring
+ * stays on the GPU's node (H2D reads it every byte), so a different storage node
+ * means O_DIRECT DMA crosses the socket link once (ref transfer.py:51-121). */
+int hl_storage_numa_node(const char* path, int32_t* node);
 
 /* Fraction of the file's pages resident in the page cache (mincore). */
 int hl_file_residency(const char* path, double* frac);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "hl_execute_plan_async": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32,
                                         C.POINTER(hl_block), C.c_uint32, C.c_void_p, C.POINTER(hl_plan_stats)]),
     "hl_ctx_cpus": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "hl_storage_numa_node": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32)]),
     "hl_topology_resolve": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                       C.c_uint32, C.POINTER(C.c_uint32)]),
     "hl_transfer_from_file": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_uint64, C.c_void_p]),
@@ -283,6 +284,13 @@ def topology_resolve(pci_bus_id: str = "", requested_node: int = -1) -> tuple[in
     arr = (C.c_int32 * max(n.value, 1))()
     check(lib.hl_topology_resolve(pci_bus_id.encode(), requested_node, C.byref(node), arr, n.value, C.byref(n)))
     return node.value, list(arr[:n.value])
+
+
+def storage_numa_node(path: str) -> int:
+    """NUMA node of the storage device holding ``path`` (hl_storage_numa_node), -1 if unknown."""
+    node = C.c_int32()
+    check(load().hl_storage_numa_node(str(path).encode(), C.byref(node)))
+    return node.value
 
 
 def file_residency(path: str) -> float:

@@ -35,6 +35,7 @@
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <sys/syscall.h>
+#include <sys/sysmacros.h>
 #include <sys/uio.h>
 #include <unistd.h>
 
@@ -169,6 +170,36 @@ static int resolve_node(const char* bus_id, int requested) {
     if (end != e && v >= 0) return (int)v;
   }
   return pci_numa_node(bus_id);
+}
+
+// NUMA node of the storage device holding `path`: /sys/dev/block/MAJ:MIN resolves
+// into the device tree; the nearest ancestor with a numa_node file (the NVMe /
+// virtio / HBA PCI function) names it. -1 when unknown (tmpfs, overlay, no sysfs).
+static int storage_numa_node(const char* path) {
+  struct stat st;
+  if (!path || stat(path, &st) != 0) return -1;
+  char rel[64];
+  snprintf(rel, sizeof rel, "/sys/dev/block/%u:%u", major(st.st_dev), minor(st.st_dev));
+  char real[4096];
+  if (!realpath(sysfs_path(rel).c_str(), real)) return -1;
+  const char* root = getenv("HL_SYSFS_ROOT");
+  char rroot[4096] = "";
+  if (root && !realpath(root, rroot)) return -1;
+  const size_t stop = strlen(rroot) + strlen("/sys/devices");
+  std::string d(real);
+  while (d.size() > stop) {
+    FILE* f = fopen((d + "/numa_node").c_str(), "r");
+    if (f) {
+      int node = -1;
+      const bool ok = fscanf(f, "%d", &node) == 1;
+      fclose(f);
+      if (ok) return node;
+    }
+    const size_t cut = d.find_last_of('/');
+    if (cut == std::string::npos || cut == 0) break;
+    d.resize(cut);
+  }
+  return -1;
 }
 
 static void pin_to(const std::vector<int>& cpus) {
@@ -1305,6 +1336,13 @@ extern "C" int hl_topology_resolve(const char* pci_bus_id, int32_t requested_nod
   const std::vector<int> c = node_cpus(*node);
   *n_cpus = (uint32_t)c.size();
   for (uint32_t i = 0; cpus && i < cap && i < c.size(); ++i) cpus[i] = c[i];
+  return HL_OK;
+}
+
+extern "C" int hl_storage_numa_node(const char* path, int32_t* node) {
+  clear_error();
+  if (!path || !node) return set_error(HL_EINVAL, "null argument");
+  *node = storage_numa_node(path);
   return HL_OK;
 }
 

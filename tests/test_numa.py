@@ -60,3 +60,27 @@ def test_engine_team_keeps_four_readers_per_rank(monkeypatch):
     assert transfer.engine_team() >= min(transfer.MIN_TEAM, transfer.DEFAULT_WORKER_CAP)
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
     assert transfer.engine_team() >= transfer.engine_team.__defaults__[0] * 0 + 1
+
+
+def test_storage_node_from_the_block_device(tmp_path, monkeypatch):
+    """hl_storage_numa_node: the file's st_dev -> /sys/dev/block/MAJ:MIN ->
+    the nearest device-tree ancestor with a numa_node (the NVMe PCI function)."""
+    path = tmp_path / "f.bin"
+    path.write_bytes(b"x")
+    st = os.stat(path)
+    root = tmp_path / "fake"
+    pci = root / "sys/devices/pci0000:80/0000:80:01.0"
+    blk = pci / "nvme/nvme1/nvme1n1"
+    blk.mkdir(parents=True)
+    (pci / "numa_node").write_text("1\n")
+    links = root / "sys/dev/block"
+    links.mkdir(parents=True)
+    (links / f"{os.major(st.st_dev)}:{os.minor(st.st_dev)}").symlink_to(
+        "../../devices/pci0000:80/0000:80:01.0/nvme/nvme1/nvme1n1")
+    monkeypatch.setenv("HL_SYSFS_ROOT", str(root))
+    assert _native.storage_numa_node(str(path)) == 1
+    (pci / "numa_node").write_text("-1\n")
+    assert _native.storage_numa_node(str(path)) == -1
+    assert _native.storage_numa_node(str(tmp_path / "missing")) == -1
+    monkeypatch.setenv("HL_SYSFS_ROOT", str(tmp_path / "nowhere"))
+    assert _native.storage_numa_node(str(path)) == -1
