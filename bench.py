@@ -848,7 +848,7 @@ def main():
         warm_cache(mapping[rank])  # "warm" means resident: O_DIRECT reads of a cold file would not make it so
         resid = residency(mapping[rank])
         for i in range(args.warmup):
-            ms, _, _, _, c = e2e_step(g, checksum=(i == args.warmup - 1))
+            ms, _, _, _, c = e2e_step(g, checksum=(world > 1 and i == args.warmup - 1))
             if c is not None:
                 csum = c
             if first_ms is None:
