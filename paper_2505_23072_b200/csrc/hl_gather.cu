@@ -1053,6 +1053,105 @@ __global__ void __launch_bounds__(kTileCastThreads) tile_cast_kernel(const __gri
   }
 }
 
+// ---------------------------------------------------------------- TMA row split (owner pack of a tensor's W column shards)
+// When a batch holds ALL W column shards of one tensor (the NCCL plane's owner
+// pack: shard w = columns [off_w, off_w+1) of every row, in order, covering the
+// row), reading each shard through its own strided box re-reads the tensor W
+// times at the source pitch in narrow bands (1 KiB of every 8 KiB row for a 7B
+// TP=8 o_proj). The split kernel reads the tensor ONCE, contiguously: one
+// elected thread streams 16 KiB source chunks HBM -> shared memory with
+// cp.async.bulk (like bulk_kernel) and writes every (row, shard) piece of the
+// chunk to its shard with a 1-D bulk store (dst_w + row * seg_w + column - off_w;
+// consecutive rows of a shard land back to back). Raw copies only; every
+// offset, width and pitch 16-byte aligned (bulk-copy rule), else tiles / rows.
+constexpr int kSplitMax = 16;  // shards per split descriptor
+struct SplitDesc {
+  uint64_t src;         // first byte of the tensor (row 0, column 0)
+  uint64_t pitch;       // bytes per source row (= sum of the shard widths)
+  uint64_t total;       // rows * pitch
+  uint64_t unit_begin;  // first 16 KiB source chunk of this descriptor in the launch
+  uint32_t nw, pad;
+  uint64_t dst[kSplitMax];       // shard w's contiguous output
+  uint32_t off[kSplitMax + 1];   // shard w = row bytes [off[w], off[w + 1])
+  uint32_t pad2;
+};
+static_assert(sizeof(SplitDesc) % 16 == 0, "SplitDesc layout");
+constexpr int kMaxSplits = 96;
+struct SplitParams {
+  uint32_t n;
+  uint32_t pad;
+  uint64_t total_units;
+  SplitDesc d[kMaxSplits];
+};
+
+__device__ __forceinline__ const SplitDesc& split_desc(const SplitParams& p, uint64_t u, uint32_t& di) {
+  while (di + 1 < p.n && p.d[di + 1].unit_begin <= u) ++di;
+  return p.d[di];
+}
+
+__global__ void __launch_bounds__(32) split_kernel(const __grid_constant__ SplitParams p) {
+  extern __shared__ __align__(128) uint8_t stage[];
+  __shared__ __align__(8) uint64_t bar[kBulkStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kBulkStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
+  uint32_t ldi = 0, sdi = 0;
+  auto load = [&](uint64_t k) {
+    const uint64_t u = first + k * step;
+    const SplitDesc& d = split_desc(p, u, ldi);
+    const uint64_t off = (u - d.unit_begin) * kBulkChunk;
+    const uint32_t bytes = (uint32_t)min((uint64_t)kBulkChunk, d.total - off);
+    const int s = (int)(k % kBulkStages);
+    const uint32_t b = smem_u32(&bar[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        :: "r"(smem_u32(stage + (size_t)s * kBulkChunk)), "l"(d.src + off), "r"(bytes), "r"(b), "l"(policy)
+        : "memory");
+  };
+  constexpr uint64_t ahead = kBulkStages - kBulkLag;
+  for (uint64_t k = 0; k < mine && k < ahead; ++k) load(k);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const uint64_t u = first + k * step;
+    const SplitDesc& d = split_desc(p, u, sdi);
+    const uint64_t a = (u - d.unit_begin) * kBulkChunk;
+    const uint64_t e = min(a + kBulkChunk, d.total);
+    const int s = (int)(k % kBulkStages);
+    const uint32_t sbase = smem_u32(stage + (size_t)s * kBulkChunk);
+    mbar_wait(smem_u32(&bar[s]), (uint32_t)((k / kBulkStages) & 1));
+    uint64_t row = a / d.pitch, col = a - row * d.pitch;
+    uint32_t w = 0;
+    while (w + 1 < d.nw && d.off[w + 1] <= col) ++w;
+    for (uint64_t x = a; x < e;) {
+      const uint64_t piece = min(e - x, (uint64_t)d.off[w + 1] - col);
+      const uint64_t seg = (uint64_t)(d.off[w + 1] - d.off[w]);
+      const uint64_t dst = d.dst[w] + row * seg + (col - d.off[w]);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                   :: "l"(dst), "r"(sbase + (uint32_t)(x - a)), "r"((uint32_t)piece), "l"(policy) : "memory");
+      x += piece;
+      col += piece;
+      if (col == d.off[w + 1]) {  // next shard, or the next row's first
+        if (++w == d.nw) {
+          w = 0;
+          col = 0;
+          ++row;
+        }
+      }
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (k + ahead < mine) {
+      asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(kBulkLag) : "memory");
+      load(k + ahead);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- host side
 static const uint32_t kSize[13] = {1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8};
 
@@ -1329,6 +1428,73 @@ static size_t tile_smem(int kind) {
   return kind == K_COPY1 ? (size_t)kTileStages * kTileBox : (size_t)2 * kTileCastStages * kTileBox;
 }
 
+// ---- TMA row split (host): a run of descriptors that is all W column shards of one tensor
+static bool splits_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HL_GATHER_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// descs[i..i+W) is a full-row split when they are raw copies of equal row
+// counts at one pitch whose source ranges follow each other and add up to the
+// pitch (so the run reads every source byte exactly once), all 16-byte aligned.
+// Returns W (0 = not a split) and fills `d` (all but unit_begin) and its units.
+static uint32_t make_split(const hl_desc* descs, uint32_t i, uint32_t n, SplitDesc& d, uint64_t& units) {
+  const hl_desc& h = descs[i];
+  if (h.src_dtype != h.dst_dtype || h.src_dtype >= 13 || h.rows < 2) return 0;
+  const uint64_t es = kSize[h.src_dtype], pitch = h.src_pitch;
+  if (!h.src || pitch % 16 || h.src % 16 || pitch >= (1ull << 32)) return 0;
+  uint64_t cum = 0;
+  uint32_t w = 0;
+  for (uint32_t j = i; j < n && w < (uint32_t)kSplitMax; ++j, ++w) {
+    const hl_desc& g = descs[j];
+    const uint64_t width = g.row_elems * es;
+    if (g.src_dtype != h.src_dtype || g.dst_dtype != h.dst_dtype || g.rows != h.rows || g.src_pitch != pitch ||
+        g.src != h.src + cum || !g.dst || g.dst % 16 || width == 0 || width % 16 || cum + width > pitch)
+      return 0;
+    d.dst[w] = g.dst;
+    d.off[w] = (uint32_t)cum;
+    cum += width;
+    if (cum == pitch) {
+      if (w == 0) return 0;  // one "shard" covering the row: a plain copy
+      d.off[w + 1] = (uint32_t)cum;
+      d.nw = w + 1;
+      d.src = h.src;
+      d.pitch = pitch;
+      d.total = h.rows * pitch;
+      units = (d.total + kBulkChunk - 1) / kBulkChunk;
+      return w + 1;
+    }
+  }
+  return 0;
+}
+
+static int launch_splits(SplitParams& p, cudaStream_t stream) {
+  if (p.total_units == 0) return HL_OK;
+  static std::mutex mu;
+  static bool attr[64] = {};
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!attr[dev & 63]) {
+      cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+      attr[dev & 63] = true;
+    }
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<uint64_t>(p.total_units, (uint64_t)sms);
+  split_kernel<<<grid, 32, kBulkSmem, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HL_ECUDA, "split launch failed: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  p.n = 0;
+  p.total_units = 0;
+  return HL_OK;
+}
+
 static int launch_tiles(int kind, TileParams& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
   static std::mutex mu;
@@ -1413,6 +1579,11 @@ extern "C" int hl_gather_prepare(int device) {
     cudaFuncGetAttributes(&a, tile_kernel_of(kind));
     cudaFuncSetAttribute(tile_kernel_of(kind), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem(kind));
   }
+  {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, split_kernel);
+    cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+  }
   encode_tiled();
   cudaGetLastError();
   cudaSetDevice(prev);
@@ -1443,7 +1614,30 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
     tile_units[k].clear();
   }
   const bool use_tiles = tma && tiles_enabled();
+  // runs of descriptors that are all W column shards of one tensor: the row split kernel
+  static thread_local std::vector<SplitDesc> splits;
+  static thread_local std::vector<uint64_t> split_units;
+  static thread_local std::vector<uint8_t> in_split;
+  splits.clear();
+  split_units.clear();
+  in_split.assign(n, 0);
+  if (tma && splits_enabled()) {
+    for (uint32_t i = 0; i < n;) {
+      SplitDesc sd;
+      uint64_t su = 0;
+      const uint32_t w = make_split(descs, i, n, sd, su);
+      if (!w) {
+        ++i;
+        continue;
+      }
+      splits.push_back(sd);
+      split_units.push_back(su);
+      for (uint32_t j = i; j < i + w; ++j) in_split[j] = 1;
+      i += w;
+    }
+  }
   for (uint32_t i = 0; i < n; ++i) {
+    if (in_split[i]) continue;
     if (use_tiles) {
       const int kind = conversion_kind(descs[i].src_dtype, descs[i].dst_dtype);
       TileDesc t;
@@ -1513,6 +1707,23 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
       i = j;
     }
     int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  if (!splits.empty()) {
+    static thread_local SplitParams* sp = nullptr;  // ~30 KB
+    if (!sp) sp = new SplitParams();
+    sp->n = 0;
+    sp->total_units = 0;
+    for (size_t i = 0; i < splits.size(); ++i) {
+      splits[i].unit_begin = sp->total_units;
+      sp->d[sp->n++] = splits[i];
+      sp->total_units += split_units[i];
+      if (sp->n == (uint32_t)kMaxSplits) {
+        int rc = launch_splits(*sp, (cudaStream_t)stream);
+        if (rc) return rc;
+      }
+    }
+    int rc = launch_splits(*sp, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return HL_OK;

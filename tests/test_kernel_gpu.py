@@ -345,3 +345,33 @@ def test_interleaved_shard_groups_across_launches(world):
     assert len(descs) > 96
     got, exp = run_both(src, cd, descs)
     assert_same(got, exp)
+
+
+@pytest.mark.parametrize("rows,cols,dt,world,lead", [
+    (4096, 4096, 10, 8, 0),      # 7B o_proj at TP=8: 1 KiB of every 8 KiB row per shard
+    (1024, 28672, 10, 8, 0),     # 70B down_proj rows (56 KiB) span several 16 KiB chunks
+    (300, 1000, 10, 8, 0),       # uneven widths (remainder columns), 16-byte aligned
+    (257, 4096, 11, 4, 16),      # f32, W=4, tensor not at the buffer start
+    (64, 2304, 1, 16, 0),        # u8, W=16: the most shards a split descriptor carries
+    (129, 96, 10, 2, 0),         # pitch smaller than a bulk chunk: one chunk holds many rows
+])
+def test_row_split_owner_pack(rows, cols, dt, world, lead):
+    """All W column shards of one tensor in a row (the NCCL plane's owner pack)
+    go to the row split kernel: the tensor is read once, contiguously, and
+    every (row, shard) piece is bulk-stored to its shard. Bit-exact against
+    the oracle with sentinels around every output, also when the run sits
+    between unrelated descriptors."""
+    rng = np.random.default_rng(rows * 7 + cols + world)
+    es = SIZES[dt]
+    src = rng.integers(0, 256, size=lead + rows * cols * es + 4096 + 64, dtype=np.uint8)
+    descs, cd = [(lead + rows * cols * es, 0, 1, 100, 100 * es, dt, dt)], ((100 * es + 15) & ~15) + 16
+    for r in range(world):
+        lo, hi = kernels.shard_bounds(cols, world, r)
+        descs.append((lead + lo * es, cd, rows, hi - lo, cols * es, dt, dt))
+        cd = (cd + rows * (hi - lo) * es + 16 + 15) & ~15  # a sentinel gap after every shard
+    descs.append((lead + 64 * es, cd, 3, 40, 200 * es, dt, dt))
+    cd += 3 * 40 * es + 64
+    l0 = _native.kernel_launches()
+    got, exp = run_both(src, cd, descs)
+    assert _native.kernel_launches() > l0
+    assert_same(got, exp)
