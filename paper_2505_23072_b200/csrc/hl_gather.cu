@@ -1064,6 +1064,7 @@ __global__ void __launch_bounds__(kTileCastThreads) tile_cast_kernel(const __gri
 // chunk to its shard with a 1-D bulk store (dst_w + row * seg_w + column - off_w;
 // consecutive rows of a shard land back to back). Raw copies only; every
 // offset, width and pitch 16-byte aligned (bulk-copy rule), else tiles / rows.
+// Off by default: see splits_enabled().
 constexpr int kSplitMax = 16;  // shards per split descriptor
 struct SplitDesc {
   uint64_t src;         // first byte of the tensor (row 0, column 0)
@@ -1429,10 +1430,14 @@ static size_t tile_smem(int kind) {
 }
 
 // ---- TMA row split (host): a run of descriptors that is all W column shards of one tensor
+// Opt-in ($HL_GATHER_SPLIT=1): measured slower than the interleaved tiles on one
+// B200 (profiles/r02_split.txt: 7B TP=8 column shards 0.59 vs 0.80 of HBM peak,
+// 70B 0.84 vs 0.98) — one thread issuing a bulk store per (row, shard) piece
+// is bound by the TMA unit's operation rate when pieces are 1-7 KiB.
 static bool splits_enabled() {
   static const bool on = [] {
     const char* e = getenv("HL_GATHER_SPLIT");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
