@@ -1060,11 +1060,13 @@ __global__ void __launch_bounds__(kTileCastThreads) tile_cast_kernel(const __gri
 // times at the source pitch in narrow bands (1 KiB of every 8 KiB row for a 7B
 // TP=8 o_proj). The split kernel reads the tensor ONCE, contiguously: one
 // elected thread streams 16 KiB source chunks HBM -> shared memory with
-// cp.async.bulk (like bulk_kernel) and writes every (row, shard) piece of the
-// chunk to its shard with a 1-D bulk store (dst_w + row * seg_w + column - off_w;
-// consecutive rows of a shard land back to back). Raw copies only; every
-// offset, width and pitch 16-byte aligned (bulk-copy rule), else tiles / rows.
-// Off by default: see splits_enabled().
+// cp.async.bulk (like bulk_kernel) and consumer warps scatter every landed
+// chunk to the shards with 16-byte streaming stores (dst_w + row * seg_w +
+// column - off_w: consecutive lanes write consecutive bytes of a shard's row).
+// Raw copies only; every offset, width and pitch 16-byte aligned, else tiles /
+// rows. (A first version issued one bulk store per (row, shard) piece from the
+// producer thread: 0.59 / 0.84 of HBM peak on 7B / 70B TP=8 column shards, bound
+// by the TMA unit's operation rate on 1-7 KiB pieces; profiles/r02_split.txt.)
 constexpr int kSplitMax = 16;  // shards per split descriptor
 struct SplitDesc {
   uint64_t src;         // first byte of the tensor (row 0, column 0)
@@ -1090,67 +1092,84 @@ __device__ __forceinline__ const SplitDesc& split_desc(const SplitParams& p, uin
   return p.d[di];
 }
 
-__global__ void __launch_bounds__(32) split_kernel(const __grid_constant__ SplitParams p) {
+constexpr int kSplitWarps = 4;   // consumer warps: scatter a landed chunk to the shards
+constexpr int kSplitStages = 6;  // 16 KiB source chunks in flight per CTA
+constexpr int kSplitCtas = 2;    // CTAs per SM
+constexpr int kSplitThreads = 32 * (1 + kSplitWarps);
+constexpr size_t kSplitSmem = (size_t)kSplitStages * kBulkChunk;
+
+__global__ void __launch_bounds__(kSplitThreads) split_kernel(const __grid_constant__ SplitParams p) {
   extern __shared__ __align__(128) uint8_t stage[];
-  __shared__ __align__(8) uint64_t bar[kBulkStages];
-  if (threadIdx.x != 0) return;
-  for (int s = 0; s < kBulkStages; ++s)
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar[s])));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  __shared__ __align__(8) uint64_t full[kSplitStages], empty[kSplitStages];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSplitStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(kSplitWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   const uint64_t first = blockIdx.x, step = gridDim.x;
   const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
-  uint32_t ldi = 0, sdi = 0;
-  auto load = [&](uint64_t k) {
-    const uint64_t u = first + k * step;
-    const SplitDesc& d = split_desc(p, u, ldi);
-    const uint64_t off = (u - d.unit_begin) * kBulkChunk;
-    const uint32_t bytes = (uint32_t)min((uint64_t)kBulkChunk, d.total - off);
-    const int s = (int)(k % kBulkStages);
-    const uint32_t b = smem_u32(&bar[s]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-        :: "r"(smem_u32(stage + (size_t)s * kBulkChunk)), "l"(d.src + off), "r"(bytes), "r"(b), "l"(policy)
-        : "memory");
-  };
-  constexpr uint64_t ahead = kBulkStages - kBulkLag;
-  for (uint64_t k = 0; k < mine && k < ahead; ++k) load(k);
+  uint32_t di = 0;
+  if (warp == 0) {  // producer: one lane streams the tensor's chunks into the stages
+    if (lane != 0) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    for (uint64_t k = 0; k < mine; ++k) {
+      const int s = (int)(k % kSplitStages);
+      if (k >= (uint64_t)kSplitStages) mbar_wait(smem_u32(&empty[s]), (uint32_t)((k / kSplitStages - 1) & 1));
+      const uint64_t u = first + k * step;
+      const SplitDesc& d = split_desc(p, u, di);
+      const uint64_t off = (u - d.unit_begin) * kBulkChunk;
+      const uint32_t bytes = (uint32_t)min((uint64_t)kBulkChunk, d.total - off);
+      const uint32_t b = smem_u32(&full[s]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+          :: "r"(smem_u32(stage + (size_t)s * kBulkChunk)), "l"(d.src + off), "r"(bytes), "r"(b), "l"(policy)
+          : "memory");
+    }
+    return;
+  }
+  // consumers: warp c scatters its contiguous quarter of the chunk, lane l the
+  // 16-byte vectors l, l + 32, ... of it (a warp step = 512 contiguous source
+  // bytes; the (row, column, shard) position advances incrementally)
+  const uint32_t c = warp - 1;
   for (uint64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % kSplitStages);
     const uint64_t u = first + k * step;
-    const SplitDesc& d = split_desc(p, u, sdi);
+    const SplitDesc& d = split_desc(p, u, di);
     const uint64_t a = (u - d.unit_begin) * kBulkChunk;
-    const uint64_t e = min(a + kBulkChunk, d.total);
-    const int s = (int)(k % kBulkStages);
-    const uint32_t sbase = smem_u32(stage + (size_t)s * kBulkChunk);
-    mbar_wait(smem_u32(&bar[s]), (uint32_t)((k / kBulkStages) & 1));
-    uint64_t row = a / d.pitch, col = a - row * d.pitch;
-    uint32_t w = 0;
-    while (w + 1 < d.nw && d.off[w + 1] <= col) ++w;
-    for (uint64_t x = a; x < e;) {
-      const uint64_t piece = min(e - x, (uint64_t)d.off[w + 1] - col);
-      const uint64_t seg = (uint64_t)(d.off[w + 1] - d.off[w]);
-      const uint64_t dst = d.dst[w] + row * seg + (col - d.off[w]);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
-                   :: "l"(dst), "r"(sbase + (uint32_t)(x - a)), "r"((uint32_t)piece), "l"(policy) : "memory");
-      x += piece;
-      col += piece;
-      if (col == d.off[w + 1]) {  // next shard, or the next row's first
-        if (++w == d.nw) {
-          w = 0;
-          col = 0;
+    const uint32_t nvec = (uint32_t)(min((uint64_t)kBulkChunk, d.total - a) / 16);
+    const uint32_t v0 = nvec * c / kSplitWarps, v1 = nvec * (c + 1) / kSplitWarps;
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kSplitStages) & 1));
+    const uint8_t* sm = stage + (size_t)s * kBulkChunk;
+    uint32_t v = v0 + lane;
+    if (v < v1) {
+      const uint64_t x = a + 16ull * v;
+      uint64_t row = x / d.pitch, col = x - row * d.pitch;
+      uint32_t w = 0;
+      while (col >= d.off[w + 1]) ++w;
+      for (;;) {
+        const uint4 val = *reinterpret_cast<const uint4*>(sm + 16ull * v);
+        const uint64_t seg = (uint64_t)(d.off[w + 1] - d.off[w]);
+        __stcs(reinterpret_cast<uint4*>(d.dst[w] + row * seg + (col - d.off[w])), val);
+        v += 32;
+        if (v >= v1) break;
+        col += 512;
+        while (col >= d.pitch) {
+          col -= d.pitch;
           ++row;
+          w = 0;
         }
+        while (col >= d.off[w + 1]) ++w;
       }
     }
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (k + ahead < mine) {
-      asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(kBulkLag) : "memory");
-      load(k + ahead);
-    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
   }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- host side
@@ -1434,12 +1453,25 @@ static size_t tile_smem(int kind) {
 // B200 (profiles/r02_split.txt: 7B TP=8 column shards 0.59 vs 0.80 of HBM peak,
 // 70B 0.84 vs 0.98) — one thread issuing a bulk store per (row, shard) piece
 // is bound by the TMA unit's operation rate when pieces are 1-7 KiB.
+// Opt-in ($HL_GATHER_SPLIT=1). Measured against the interleaved tiles on one B200
+// (profiles/r02_split*.txt): 7B TP=8 column shards 0.84 vs 0.80 of HBM peak (it
+// wins on the 2,752-byte down_proj rows the 2 KiB tile boxes cut raggedly, loses
+// on the 1 KiB o_proj rows), 70B 0.89 vs 0.98 — no width rule wins on both, so the
+// tiles stay the default. $HL_SPLIT_MAX_SEG caps the shard width it takes.
 static bool splits_enabled() {
   static const bool on = [] {
     const char* e = getenv("HL_GATHER_SPLIT");
     return e && e[0] == '1';
   }();
   return on;
+}
+
+static uint64_t split_max_seg() {
+  static const uint64_t v = [] {
+    const char* e = getenv("HL_SPLIT_MAX_SEG");
+    return e ? strtoull(e, nullptr, 10) : ~0ull;
+  }();
+  return v;
 }
 
 // descs[i..i+W) is a full-row split when they are raw copies of equal row
@@ -1457,7 +1489,8 @@ static uint32_t make_split(const hl_desc* descs, uint32_t i, uint32_t n, SplitDe
     const hl_desc& g = descs[j];
     const uint64_t width = g.row_elems * es;
     if (g.src_dtype != h.src_dtype || g.dst_dtype != h.dst_dtype || g.rows != h.rows || g.src_pitch != pitch ||
-        g.src != h.src + cum || !g.dst || g.dst % 16 || width == 0 || width % 16 || cum + width > pitch)
+        g.src != h.src + cum || !g.dst || g.dst % 16 || width == 0 || width % 16 || cum + width > pitch ||
+        width > split_max_seg())
       return 0;
     d.dst[w] = g.dst;
     d.off[w] = (uint32_t)cum;
@@ -1485,13 +1518,13 @@ static int launch_splits(SplitParams& p, cudaStream_t stream) {
   {
     std::lock_guard<std::mutex> g(mu);
     if (!attr[dev & 63]) {
-      cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+      cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem);
       attr[dev & 63] = true;
     }
   }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<uint64_t>(p.total_units, (uint64_t)sms);
-  split_kernel<<<grid, 32, kBulkSmem, stream>>>(p);
+  const unsigned grid = (unsigned)std::min<uint64_t>(p.total_units, (uint64_t)sms * kSplitCtas);
+  split_kernel<<<grid, kSplitThreads, kSplitSmem, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HL_ECUDA, "split launch failed: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
@@ -1587,7 +1620,7 @@ extern "C" int hl_gather_prepare(int device) {
   {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, split_kernel);
-    cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+    cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem);
   }
   encode_tiled();
   cudaGetLastError();
