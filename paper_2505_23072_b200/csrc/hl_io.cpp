@@ -653,7 +653,7 @@ struct Uring {
   size_t sq_sz = 0, cq_sz = 0, sqe_sz = 0;
   io_uring_sqe* sqes = nullptr;
   io_uring_cqe* cqes = nullptr;
-  unsigned *sq_tail = nullptr, *sq_mask = nullptr, *sq_array = nullptr;
+  unsigned *sq_head = nullptr, *sq_tail = nullptr, *sq_mask = nullptr, *sq_array = nullptr;
   unsigned *cq_head = nullptr, *cq_tail = nullptr, *cq_mask = nullptr;
 
   bool open(unsigned entries) {
@@ -671,6 +671,7 @@ struct Uring {
     cq = b == MAP_FAILED ? nullptr : (uint8_t*)b;
     sqes = c == MAP_FAILED ? nullptr : (io_uring_sqe*)c;
     if (!sq || !cq || !sqes) return false;
+    sq_head = (unsigned*)(sq + p.sq_off.head);
     sq_tail = (unsigned*)(sq + p.sq_off.tail);
     sq_mask = (unsigned*)(sq + p.sq_off.ring_mask);
     sq_array = (unsigned*)(sq + p.sq_off.array);
@@ -700,9 +701,11 @@ struct Uring {
     sq_array[idx] = idx;
     __atomic_store_n(sq_tail, tail + 1, __ATOMIC_RELEASE);
   }
-  // submit `n` queued reads, wait for at least `wait` completions
-  int enter(unsigned n, unsigned wait) {
+  // submit every queued read the kernel has not consumed yet (a partial submit
+  // leaves the rest for the next call), wait for at least `wait` completions
+  int enter(unsigned wait) {
     for (;;) {
+      const unsigned n = *sq_tail - __atomic_load_n(sq_head, __ATOMIC_ACQUIRE);
       int r = (int)syscall(__NR_io_uring_enter, fd, n, wait, wait ? IORING_ENTER_GETEVENTS : 0, nullptr, 0);
       if (r >= 0 || errno != EINTR) return r < 0 ? -errno : r;
     }
@@ -796,11 +799,12 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
     }
     return -1;
   };
-  while (!run->failed.load(std::memory_order_relaxed)) {
-    unsigned queued = 0;
-    while (claiming && inflight < depth) {
+  // Every exit goes through the drain at the end: reads in flight target our
+  // pinned slots, so none may still be running when the slots are handed on.
+  for (;;) {
+    while (claiming && inflight < depth && !run->failed.load(std::memory_order_relaxed)) {
       const long si = free_slot(inflight == 0);
-      if (si < 0) break;  // wait for completions first
+      if (si < 0) break;  // wait for completions first (or a failed DMA wait)
       const size_t i = run->cursor.fetch_add(1);
       if (i >= chunks.size()) {
         claiming = false;
@@ -826,11 +830,11 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
         if (!pread_full(f.bfd, s.host + head, c.len, c.off, &got, &err) || got < c.len) {
           run->fail(HL_EIO, err ? std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err)
                                 : "unexpected EOF at file offset " + std::to_string(c.off + got));
-          return;
+          break;
         }
         run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
         run->buffered_bytes += c.len;
-        if (!h2d(s, c, head)) return;
+        if (!h2d(s, c, head)) break;
         continue;
       }
       Req& q = req[si];
@@ -839,18 +843,17 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
       q.alen = round_up(c.off + c.len, kAlign) - q.aoff;
       q.reading = true;
       ring.read(f.dfd, s.host, (uint32_t)q.alen, q.aoff, (uint64_t)si);
-      ++queued;
       ++inflight;
     }
+    if (run->failed.load(std::memory_order_relaxed)) claiming = false;  // stop claiming, reap what is in flight
     if (!claiming && inflight == 0) break;
     const double tr = now_s();
-    const int r = ring.enter(queued, inflight ? 1 : 0);
+    const int r = ring.enter(inflight ? 1 : 0);  // always submits what was queued
     run->read_ns += (uint64_t)((now_s() - tr) * 1e9);
     if (r < 0) {
       run->fail(HL_EIO, std::string("io_uring_enter: ") + strerror(-r));
-      return;
+      break;
     }
-    bool ok = true;
     ring.reap([&](uint64_t tag, int res) {
       Req& q = req[tag];
       Slot& s = *slots[tag];
@@ -858,7 +861,7 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
       FileState& f = files[c.file];
       q.reading = false;
       --inflight;
-      if (!ok) return;
+      if (run->failed.load(std::memory_order_relaxed)) return;  // draining after a failure
       const uint64_t head = c.off % kAlign;
       const uint64_t need = c.off + c.len - q.aoff;  // bytes the chunk needs from the aligned start
       uint64_t got = res > 0 ? (uint64_t)res : 0;
@@ -867,12 +870,11 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
         err = 0;
         uint64_t n = 0;
         if (!pread_full(f.bfd, s.host + head, c.len, c.off, &n, &err) || n < c.len) {
-          ok = false;
           run->fail(HL_EIO, "read failed at offset " + std::to_string(c.off));
           return;
         }
         run->buffered_bytes += c.len;
-        ok = h2d(s, c, head);
+        h2d(s, c, head);
         return;
       }
       if (!err && got < need && got % kAlign == 0) {  // short read: finish it synchronously
@@ -880,19 +882,17 @@ static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
         if (pread_full(f.dfd, s.host + got, q.alen - got, q.aoff + got, &n, &err)) got += n;
       }
       if (err || got < need) {
-        ok = false;
         run->fail(HL_EIO, err ? std::string("read failed at offset ") + std::to_string(c.off) + ": " + strerror(err)
                               : "unexpected EOF at file offset " + std::to_string(q.aoff + got));
         return;
       }
       run->direct_bytes += c.len;
       run->uring_bytes += c.len;
-      ok = h2d(s, c, head);
+      h2d(s, c, head);
     });
-    if (!ok) break;
   }
-  // a failure can leave reads in flight into our slots: let them land before the slots are reused
-  while (inflight > 0 && ring.enter(0, 1) >= 0) ring.reap([&](uint64_t tag, int) {
+  // reads still in flight after a failure land in our slots before they are handed on
+  while (inflight > 0 && ring.enter(1) >= 0) ring.reap([&](uint64_t tag, int) {
       req[tag].reading = false;
       --inflight;
     });
