@@ -68,8 +68,6 @@ def parse():
     ap.add_argument("--cold-steps", type=int, default=2, help="e2e steps after dropping the page cache (0: none)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--quick", action="store_true", help="skip io probes, cpu baseline and the fresh-process load")
-    ap.add_argument("--baselines", type=int, default=0,
-                    help="also time upstream fastsafetensors and safetensors on the same files (N=1)")
     ap.add_argument("--files", type=int, default=0,
                     help="re-split the checkpoint into this many files (0: HF split at N=1, N files at N>1)")
     ap.add_argument("--layers", type=int, default=None,
@@ -484,62 +482,6 @@ def io_probes(paths, device_index: int) -> dict:
     return out
 
 
-def library_baselines(paths, device_index: int, tensor_bytes: int, steps: int = 3) -> dict:
-    """Same files, same box, warm page cache, every key ready on the GPU
-    (median of ``steps`` after one warm-up): upstream fastsafetensors 0.3.1
-    from the image (GDS off: no nvidia-fs) and safetensors load_file."""
-    import torch
-
-    dev = f"cuda:{device_index}"
-    out = {}
-
-    def timed(fn, n):
-        ts = []
-        for i in range(n + 1):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            fn()
-            torch.cuda.synchronize()
-            if i:
-                ts.append(time.perf_counter() - t0)
-        return statistics.median(ts)
-
-    try:
-        import fastsafetensors
-        from fastsafetensors import SafeTensorsFileLoader as FstLoader
-
-        def fst():
-            ld = FstLoader(None, dev, nogds=True)
-            ld.add_filenames({0: [str(p) for p in paths]})
-            fb = ld.copy_files_to_device()
-            ts = [fb.get_tensor(k) for k in ld.get_keys()]
-            torch.cuda.synchronize()
-            del ts
-            fb.close()
-            ld.close()
-
-        t = timed(fst, steps)
-        out["fastsafetensors"] = {"version": getattr(fastsafetensors, "__version__", "0.3.1"), "mode": "nogds",
-                                  "value": round(tensor_bytes / t / 1e9, 3), "unit": "GB/s", "seconds": round(t, 4)}
-    except Exception as e:  # noqa: BLE001 - a baseline that cannot run is reported, not fatal
-        out["fastsafetensors"] = {"error": f"{type(e).__name__}: {e}"[:200]}
-    try:
-        import safetensors
-        from safetensors.torch import load_file
-
-        def st():
-            ts = [load_file(str(p), device=dev) for p in paths]
-            torch.cuda.synchronize()
-            del ts
-
-        t = timed(st, max(1, steps - 1))
-        out["safetensors"] = {"version": safetensors.__version__, "call": "load_file(device=cuda)",
-                              "value": round(tensor_bytes / t / 1e9, 3), "unit": "GB/s", "seconds": round(t, 4)}
-    except Exception as e:  # noqa: BLE001
-        out["safetensors"] = {"error": f"{type(e).__name__}: {e}"[:200]}
-    return out
-
-
 FRESH = r"""
 import json, sys, time
 sys.path.insert(0, {root!r})
@@ -918,11 +860,9 @@ def main():
                 "buffered_bytes": st.buffered_bytes if st else None}
         warm_cache(mapping[rank])
 
-    cpu = libs = fresh = None
+    cpu = fresh = None
     if rank == 0 and world == 1 and not args.quick:
         fresh = e2e_fresh_process(paths, local, args.backend, job_bytes) if cast is None else None
-        if args.baselines:
-            libs = library_baselines(paths, local, tensor_bytes)
         if args.cpu_baseline:
             cpu = run_cpu_reference(paths, keys, policy, steps=1, warmup=0, cold_steps=1 if args.cold_steps else 0,
                                     cast=cast)
@@ -956,7 +896,6 @@ def main():
             "e2e_cold": cold,
             "planes": plane_out if world > 1 else None,
             "e2e_fresh_process": fresh,
-            "library_baselines": libs,
             "roofline": roofline,
             "io_roofline": io,
             "io_mode_cufile": ("measured: see e2e io_modes" if gds
