@@ -21,7 +21,9 @@ for i in range(12):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t0 = time.perf_counter()
     ev[0].record()
-    ld = SafeTensorsFileLoader(SingleGroup(), "cuda:0", config=LoaderConfig(auto_release=True))
+    bounce = int(os.environ.get("HL_PROBE_BOUNCE", "0"))  # engine slot size (LoaderConfig.host_bounce_bytes)
+    cfg = LoaderConfig(auto_release=True, **({"host_bounce_bytes": bounce} if bounce else {}))
+    ld = SafeTensorsFileLoader(SingleGroup(), "cuda:0", config=cfg)
     ld.add_filenames({0: paths})
     t1 = time.perf_counter()
     fb = ld.copy_files_to_device()
