@@ -596,3 +596,35 @@ def test_kept_small_outputs_pin_a_small_chunk(tmp_path, rng):
     loader.close()
     assert kept.untyped_storage().nbytes() == device.CARVE_SMALL_CHUNK
     assert kept.view(torch.uint8).cpu().numpy().tobytes() == t["n0"][2]
+
+
+@pytest.mark.parametrize("residue", [1, 3, 481])
+def test_realign_in_place_under_a_tight_device_cap(tmp_path, rng, residue, monkeypatch):
+    """An odd header on the simdirect landing needs the realign; with a
+    device_cap that holds the landing buffer but not a second copy, the loader
+    repacks inside the landing buffer like the reference (device.py:466-534)
+    instead of raising OutOfMemory — through small scratch windows here, so the
+    overlapping (shift < window) and disjoint piece paths both run. Bytes are
+    the file's (oracle)."""
+    from paper_2505_23072_b200 import loader as loader_mod
+
+    monkeypatch.setattr(loader_mod, "REPACK_WINDOW", 4096)
+    t = {"a": (DType.F32, (3000,), rng.integers(0, 256, 12000, dtype=np.uint8).tobytes()),
+         "b": (DType.BF16, (7, 5), rng.integers(0, 256, 70, dtype=np.uint8).tobytes()),
+         "c": (DType.F64, (1001,), rng.integers(0, 256, 8008, dtype=np.uint8).tobytes()),
+         "d": (DType.U8, (5,), rng.integers(0, 256, 5, dtype=np.uint8).tobytes())}
+    p = _write(tmp_path, "odd.safetensors", t, pad=pad_for_body_residue(t, residue))
+    probe = SafeTensorsFileLoader(SingleGroup(), "simdirect")
+    probe.add_filenames({0: [p]})
+    fb = probe.copy_files_to_device()
+    cap = fb.transferred_buffer_bytes * 3 // 2  # room for the landing buffer, not for a second copy
+    fb.close()
+    probe.close()
+    ld = SafeTensorsFileLoader(SingleGroup(), "simdirect", config=LoaderConfig(device_cap=cap, auto_release=False))
+    ld.add_filenames({0: [p]})
+    fb = ld.copy_files_to_device()
+    for k, (_, _, raw) in t.items():
+        assert fb.get_tensor(k).tobytes() == raw, k
+    assert ld.pool.allocated_bytes <= cap
+    fb.close()
+    ld.close()
