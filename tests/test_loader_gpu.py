@@ -610,7 +610,7 @@ def test_realign_in_place_under_a_tight_device_cap(tmp_path, rng, residue, monke
 
     monkeypatch.setattr(loader_mod, "REPACK_WINDOW", 4096)
     t = {"a": (DType.F32, (3000,), rng.integers(0, 256, 12000, dtype=np.uint8).tobytes()),
-         "b": (DType.BF16, (7, 5), rng.integers(0, 256, 70, dtype=np.uint8).tobytes()),
+         "b": (DType.BF16, (7, 4), rng.integers(0, 256, 56, dtype=np.uint8).tobytes()),  # writer-aligned begins
          "c": (DType.F64, (1001,), rng.integers(0, 256, 8008, dtype=np.uint8).tobytes()),
          "d": (DType.U8, (5,), rng.integers(0, 256, 5, dtype=np.uint8).tobytes())}
     p = _write(tmp_path, "odd.safetensors", t, pad=pad_for_body_residue(t, residue))
