@@ -7,7 +7,7 @@
 #   C5 Bloom-176B bf16, first 8 blocks (disk), on-device fp16 cast; cold leg included
 mkdir -p gpurun_out
 D=${HL_BENCH_DIR:-/tmp/hl_bench}
-T=${T:-1200}
+T=${T:-1500}
 run() { local name=$1; shift; timeout $T "$@" > gpurun_out/cfg_$name.log 2>&1; echo "$name exit $?"; }
 run c1 python bench.py --arch gpt2 --steps 5 --warmup 3
 run c1_odd_gds python bench.py --arch gpt2 --header odd --backend gds --steps 5 --warmup 3

@@ -1,6 +1,6 @@
 // storage_probe.c — how fast can this box's storage deliver a cold file?
-// O_DIRECT reads, (a) T threads of synchronous pread, (b) one io_uring ring at
-// queue depth Q (raw syscalls, no liburing). Prints one JSON line per config.
+// O_DIRECT reads, (a) T threads of synchronous pread, (b) io_uring rings (one per
+// thread) at queue depth Q (raw syscalls, no liburing). Prints one JSON line per config.
 //   gcc -O2 -pthread -o /tmp/storage_probe tools/storage_probe.c
 //   /tmp/storage_probe FILE... [quick]  (reads all FILEs as one job, dropped from the page
 //                                        cache before each run; quick: two configs only)
@@ -100,15 +100,19 @@ static int uring_enter(int fd, unsigned submit, unsigned wait, unsigned flags) {
   return (int)syscall(__NR_io_uring_enter, fd, submit, wait, flags, NULL, 0);
 }
 
-static void uring(unsigned qd, uint64_t chunk) {
-  drop();
+static unsigned g_qd;
+
+// one io_uring ring at depth g_qd; chunks claimed from the shared cursor (several
+// threads = several rings, as the engine's cold reader runs)
+static void* uring_worker(void* arg) {
+  int* failed = (int*)arg;
   struct io_uring_params p;
   memset(&p, 0, sizeof p);
+  const unsigned qd = g_qd;
   int rfd = uring_setup(qd, &p);
   if (rfd < 0) {
-    printf("{\"probe\": \"io_uring\", \"error\": \"io_uring_setup failed (%s)\"}\n", strerror(-rfd > 0 ? -rfd : 1));
-    fflush(stdout);
-    return;
+    *failed = 1;
+    return NULL;
   }
   size_t sq_sz = p.sq_off.array + p.sq_entries * sizeof(unsigned);
   size_t cq_sz = p.cq_off.cqes + p.cq_entries * sizeof(struct io_uring_cqe);
@@ -125,59 +129,86 @@ static void uring(unsigned qd, uint64_t chunk) {
   struct io_uring_cqe* cqes = (struct io_uring_cqe*)(cq + p.cq_off.cqes);
   int fds[MAXF];
   for (int i = 0; i < g_nfiles; ++i) fds[i] = open(g_paths[i], O_RDONLY | O_DIRECT);
-  uint8_t* bufs;
-  bufs = (uint8_t*)big_buffer((size_t)qd * chunk);
-  if (!bufs) return;
-  uint64_t next = 0, done = 0;
-  unsigned inflight = 0;
-  double t0 = now();
+  uint8_t* bufs = (uint8_t*)big_buffer((size_t)qd * g_chunk);
+  if (!bufs) {
+    *failed = 1;
+    return NULL;
+  }
   unsigned free_slots[1024];
-  unsigned nfree = qd;
+  unsigned nfree = qd, inflight = 0;
+  int claiming = 1;
   for (unsigned i = 0; i < qd; ++i) free_slots[i] = i;
-  while (done < g_size) {
+  while (claiming || inflight) {
     unsigned queued = 0;
-    while (nfree && next < g_size) {
+    while (claiming && nfree) {
+      uint64_t off = atomic_fetch_add(&g_cursor, g_chunk);
+      if (off >= g_size) {
+        claiming = 0;
+        break;
+      }
+      uint64_t local;
+      const int f = locate(off, &local);
+      uint64_t n = g_sizes[f] - local < g_chunk ? g_sizes[f] - local : g_chunk;
       unsigned slot = free_slots[--nfree];
       unsigned tail = *sq_tail;
       unsigned idx = tail & *sq_mask;
       struct io_uring_sqe* e = &sqes[idx];
       memset(e, 0, sizeof *e);
-      uint64_t local;
-      const int f = locate(next, &local);
-      uint64_t n = g_sizes[f] - local < chunk ? g_sizes[f] - local : chunk;
       e->opcode = IORING_OP_READ;
       e->fd = fds[f];
-      e->addr = (uint64_t)(uintptr_t)(bufs + (size_t)slot * chunk);
+      e->addr = (uint64_t)(uintptr_t)(bufs + (size_t)slot * g_chunk);
       e->len = (uint32_t)n;
       e->off = local;
-      e->user_data = ((uint64_t)slot << 40) | n;
+      e->user_data = slot;
       sq_array[idx] = idx;
       __atomic_store_n(sq_tail, tail + 1, __ATOMIC_RELEASE);
-      next += n;
       ++queued;
       ++inflight;
     }
-    int r = uring_enter(rfd, queued, 1, IORING_ENTER_GETEVENTS);
-    if (r < 0) break;
+    if (!inflight) break;
+    if (uring_enter(rfd, queued, 1, IORING_ENTER_GETEVENTS) < 0) {
+      *failed = 1;
+      break;
+    }
     unsigned head = *cq_head;
     while (head != __atomic_load_n(cq_tail, __ATOMIC_ACQUIRE)) {
       struct io_uring_cqe* c = &cqes[head & *cq_mask];
-      if (c->res < 0) { printf("{\"probe\": \"io_uring\", \"error\": \"read failed %d\"}\n", c->res); return; }
-      done += c->user_data & ((1ull << 40) - 1);
-      free_slots[nfree++] = (unsigned)(c->user_data >> 40);
+      if (c->res < 0) *failed = 1;
+      free_slots[nfree++] = (unsigned)c->user_data;
       --inflight;
       ++head;
     }
     __atomic_store_n(cq_head, head, __ATOMIC_RELEASE);
   }
-  double dt = now() - t0;
-  printf("{\"probe\": \"io_uring\", \"qd\": %u, \"chunk_mb\": %.2f, \"GBps\": %.3f}\n", qd, chunk / 1048576.0,
-         g_size / dt / 1e9);
-  fflush(stdout);
   for (int i = 0; i < g_nfiles; ++i) close(fds[i]);
   close(rfd);
   free(bufs);
+  return NULL;
 }
+
+static void uring_threads(int t, unsigned qd, uint64_t chunk) {
+  drop();
+  g_chunk = chunk;
+  g_qd = qd;
+  atomic_store(&g_cursor, 0);
+  pthread_t th[64];
+  int failed[64] = {0};
+  double t0 = now();
+  for (int i = 0; i < t; ++i) pthread_create(&th[i], NULL, uring_worker, &failed[i]);
+  for (int i = 0; i < t; ++i) pthread_join(th[i], NULL);
+  double dt = now() - t0;
+  int bad = 0;
+  for (int i = 0; i < t; ++i) bad |= failed[i];
+  if (bad) {
+    printf("{\"probe\": \"io_uring\", \"threads\": %d, \"qd\": %u, \"error\": \"io_uring setup or read failed\"}\n", t, qd);
+  } else {
+    printf("{\"probe\": \"io_uring\", \"threads\": %d, \"qd\": %u, \"chunk_mb\": %.2f, \"GBps\": %.3f}\n", t, qd,
+           chunk / 1048576.0, g_size / dt / 1e9);
+  }
+  fflush(stdout);
+}
+
+static void uring(unsigned qd, uint64_t chunk) { uring_threads(1, qd, chunk); }
 
 int main(int argc, char** argv) {
   int quick = 0;
@@ -211,5 +242,7 @@ int main(int argc, char** argv) {
   uring(128, 1 << 20);
   uring(128, 512 << 10);
   uring(64, 4 << 20);
+  uring_threads(2, 16, 1 << 20);  // the engine's cold reader: 2 rings x 16 x 1 MiB
+  uring_threads(4, 8, 1 << 20);
   return 0;
 }
