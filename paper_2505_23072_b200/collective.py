@@ -121,21 +121,30 @@ def _source_ptr(view, device: torch.device) -> tuple[int, bool]:
 
 
 def pack_parts(spec: ShardSpec, src_ptr: int, in_dtype: DType, out_dtype: DType, own: int,
-               own_out: torch.Tensor, device: torch.device) -> list[torch.Tensor]:
+               own_out: torch.Tensor, device: torch.device, src_bytes: torch.Tensor | None = None) -> list[torch.Tensor]:
     """Owner-side pack of the NCCL scatter: every rank's slice of the tensor at
     ``src_ptr`` (cast to ``out_dtype``) with ONE hl_gather launch — the owner's
     own slice straight into ``own_out``, the others into one pack buffer with
-    16-byte aligned parts. Returns the W uint8 parts, enqueued on the current
-    stream (ref collective.py:214-255 / 318-330)."""
+    16-byte aligned parts. A part that is one contiguous range of the source
+    (dim 0, or only size-1 dims before ``dim``) with no cast is sent straight
+    from the source bytes (``src_bytes``: a uint8 tensor starting at
+    ``src_ptr``), as SURVEY §8e specifies: no pack copy. Returns the W uint8
+    parts, enqueued on the current stream (ref collective.py:214-255 / 318-330)."""
     esz = out_dtype.size_bytes
     sizes = [math.prod(p) * esz for p in spec.part_shapes]
-    pack_bytes = sum(-(-sz // 16) * 16 for r, sz in enumerate(sizes) if r != own)
-    pack = torch.empty(pack_bytes + 16, dtype=torch.uint8, device=device)
+    contiguous = math.prod(spec.full_shape[:spec.dim]) == 1 and in_dtype is out_dtype and src_bytes is not None
+    inner = math.prod(spec.full_shape[spec.dim + 1:]) * in_dtype.size_bytes
+    packed = [r for r in range(spec.world_size) if r != own and not contiguous]
+    pack_bytes = sum(-(-sizes[r] // 16) * 16 for r in packed)
+    pack = torch.empty(pack_bytes + 16, dtype=torch.uint8, device=device) if packed else None
     parts, descs, cursor = [], [], 0
     for r in range(spec.world_size):
         lo, hi = spec.bounds(r)
         if r == own:
             dst, part = own_out.data_ptr(), own_out
+        elif contiguous:
+            parts.append(src_bytes[lo * inner:lo * inner + sizes[r]])
+            continue
         else:
             dst, part = pack.data_ptr() + cursor, pack[cursor : cursor + sizes[r]]
             cursor += -(-sizes[r] // 16) * 16  # keep every part 16-byte aligned
@@ -593,7 +602,9 @@ class DistGroup:
             raise SpecMismatch(f"scatter src rank {src} holds no view (tag={tag!r})")
         if tuple(source_view.shape) != spec.full_shape:
             raise SpecMismatch(f"source shape {list(source_view.shape)} does not match spec {list(spec.full_shape)}")
+        t = source_view.buffer.tensor
         parts = pack_parts(spec, source_view.buffer.ptr + source_view.base_offset, in_dtype, out_dtype,
-                           own=src, own_out=mine, device=pool.device)
+                           own=src, own_out=mine, device=pool.device,
+                           src_bytes=t[source_view.base_offset:source_view.base_offset + source_view.nbytes])
         self.scatter_parts(rank, src, parts, mine)
         return out

@@ -199,6 +199,14 @@ def test_nccl_plane_owner_pack(world, dim, cast):
         _, exp = oracle.slice_bytes(src_bytes, out_dt.value, shape, dim, world, r)
         assert parts[r].cpu().numpy().tobytes() == exp, (r, dim, world, cast)
     assert parts[own].data_ptr() == own_out.data_ptr()
+    # with the source bytes at hand, a part that is one contiguous source range (dim 0, no
+    # cast) is sent straight from the source: no pack copy, same bytes
+    parts = pack_parts(spec, s.data_ptr() + 5, DType.BF16, out_dt, own, own_out, dev, src_bytes=s[5:5 + raw.size])
+    for r in range(world):
+        _, exp = oracle.slice_bytes(src_bytes, out_dt.value, shape, dim, world, r)
+        assert parts[r].cpu().numpy().tobytes() == exp, ("direct", r, dim, world, cast)
+        in_source = s.data_ptr() <= parts[r].data_ptr() < s.data_ptr() + s.numel()
+        assert in_source == (r != own and dim == 0 and not cast), (r, dim, cast)
 
 
 @pytest.mark.parametrize("seed", range(4))
