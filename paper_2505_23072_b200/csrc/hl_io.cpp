@@ -724,6 +724,17 @@ struct Uring {
   }
 };
 
+// io_uring usable in this process (kernel support, not disabled by sysctl or a
+// seccomp filter): probed once. Without it cold plans keep the blocking readers
+// of the whole cold team instead of 2 threads falling back to one read each.
+static bool uring_available() {
+  static const bool ok = [] {
+    Uring r;
+    return r.open(2);
+  }();
+  return ok;
+}
+
 static void uring_loop(PlanRun* run, uint32_t u, WorkerRing& home) {
   hl_ctx* ctx = run->ctx;
   const auto& chunks = *run->chunks;
@@ -1249,7 +1260,8 @@ static int execute(hl_ctx* ctx, const char* const* paths, uint32_t n_files, cons
   // $HL_URING_THREADS threads x $HL_URING_DEPTH reads in flight, using the slots
   // of the whole cold team. cuFile / mmap plans keep their own paths.
   const char* ue = getenv("HL_COLD_URING");
-  if (cold_plan && !(ue && ue[0] == '0') && !(mode_mask & ((1u << HL_IO_CUFILE) | (1u << HL_IO_MMAP)))) {
+  if (cold_plan && !(ue && ue[0] == '0') && !(mode_mask & ((1u << HL_IO_CUFILE) | (1u << HL_IO_MMAP))) &&
+      uring_available()) {
     auto env_u32 = [](const char* name, long dflt, long lo, long hi) {
       const char* v = getenv(name);
       return (uint32_t)std::max(lo, std::min(v ? strtol(v, nullptr, 10) : dflt, hi));
