@@ -1053,125 +1053,6 @@ __global__ void __launch_bounds__(kTileCastThreads) tile_cast_kernel(const __gri
   }
 }
 
-// ---------------------------------------------------------------- TMA row split (owner pack of a tensor's W column shards)
-// When a batch holds ALL W column shards of one tensor (the NCCL plane's owner
-// pack: shard w = columns [off_w, off_w+1) of every row, in order, covering the
-// row), reading each shard through its own strided box re-reads the tensor W
-// times at the source pitch in narrow bands (1 KiB of every 8 KiB row for a 7B
-// TP=8 o_proj). The split kernel reads the tensor ONCE, contiguously: one
-// elected thread streams 16 KiB source chunks HBM -> shared memory with
-// cp.async.bulk (like bulk_kernel) and consumer warps scatter every landed
-// chunk to the shards with 16-byte streaming stores (dst_w + row * seg_w +
-// column - off_w: consecutive lanes write consecutive bytes of a shard's row).
-// Raw copies only; every offset, width and pitch 16-byte aligned, else tiles /
-// rows. (A first version issued one bulk store per (row, shard) piece from the
-// producer thread: 0.59 / 0.84 of HBM peak on 7B / 70B TP=8 column shards, bound
-// by the TMA unit's operation rate on 1-7 KiB pieces; profiles/r02_split.txt.)
-constexpr int kSplitMax = 16;  // shards per split descriptor
-struct SplitDesc {
-  uint64_t src;         // first byte of the tensor (row 0, column 0)
-  uint64_t pitch;       // bytes per source row (= sum of the shard widths)
-  uint64_t total;       // rows * pitch
-  uint64_t unit_begin;  // first 16 KiB source chunk of this descriptor in the launch
-  uint32_t nw, pad;
-  uint64_t dst[kSplitMax];       // shard w's contiguous output
-  uint32_t off[kSplitMax + 1];   // shard w = row bytes [off[w], off[w + 1])
-  uint32_t pad2;
-};
-static_assert(sizeof(SplitDesc) % 16 == 0, "SplitDesc layout");
-constexpr int kMaxSplits = 96;
-struct SplitParams {
-  uint32_t n;
-  uint32_t pad;
-  uint64_t total_units;
-  SplitDesc d[kMaxSplits];
-};
-
-__device__ __forceinline__ const SplitDesc& split_desc(const SplitParams& p, uint64_t u, uint32_t& di) {
-  while (di + 1 < p.n && p.d[di + 1].unit_begin <= u) ++di;
-  return p.d[di];
-}
-
-constexpr int kSplitWarps = 4;   // consumer warps: scatter a landed chunk to the shards
-constexpr int kSplitStages = 6;  // 16 KiB source chunks in flight per CTA
-constexpr int kSplitCtas = 2;    // CTAs per SM
-constexpr int kSplitThreads = 32 * (1 + kSplitWarps);
-constexpr size_t kSplitSmem = (size_t)kSplitStages * kBulkChunk;
-
-__global__ void __launch_bounds__(kSplitThreads) split_kernel(const __grid_constant__ SplitParams p) {
-  extern __shared__ __align__(128) uint8_t stage[];
-  __shared__ __align__(8) uint64_t full[kSplitStages], empty[kSplitStages];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSplitStages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(kSplitWarps));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint64_t first = blockIdx.x, step = gridDim.x;
-  const uint64_t mine = first < p.total_units ? (p.total_units - first + step - 1) / step : 0;
-  uint32_t di = 0;
-  if (warp == 0) {  // producer: one lane streams the tensor's chunks into the stages
-    if (lane != 0) return;
-    uint64_t policy;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-    for (uint64_t k = 0; k < mine; ++k) {
-      const int s = (int)(k % kSplitStages);
-      if (k >= (uint64_t)kSplitStages) mbar_wait(smem_u32(&empty[s]), (uint32_t)((k / kSplitStages - 1) & 1));
-      const uint64_t u = first + k * step;
-      const SplitDesc& d = split_desc(p, u, di);
-      const uint64_t off = (u - d.unit_begin) * kBulkChunk;
-      const uint32_t bytes = (uint32_t)min((uint64_t)kBulkChunk, d.total - off);
-      const uint32_t b = smem_u32(&full[s]);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-          :: "r"(smem_u32(stage + (size_t)s * kBulkChunk)), "l"(d.src + off), "r"(bytes), "r"(b), "l"(policy)
-          : "memory");
-    }
-    return;
-  }
-  // consumers: warp c scatters its contiguous quarter of the chunk, lane l the
-  // 16-byte vectors l, l + 32, ... of it (a warp step = 512 contiguous source
-  // bytes; the (row, column, shard) position advances incrementally)
-  const uint32_t c = warp - 1;
-  for (uint64_t k = 0; k < mine; ++k) {
-    const int s = (int)(k % kSplitStages);
-    const uint64_t u = first + k * step;
-    const SplitDesc& d = split_desc(p, u, di);
-    const uint64_t a = (u - d.unit_begin) * kBulkChunk;
-    const uint32_t nvec = (uint32_t)(min((uint64_t)kBulkChunk, d.total - a) / 16);
-    const uint32_t v0 = nvec * c / kSplitWarps, v1 = nvec * (c + 1) / kSplitWarps;
-    mbar_wait(smem_u32(&full[s]), (uint32_t)((k / kSplitStages) & 1));
-    const uint8_t* sm = stage + (size_t)s * kBulkChunk;
-    uint32_t v = v0 + lane;
-    if (v < v1) {
-      const uint64_t x = a + 16ull * v;
-      uint64_t row = x / d.pitch, col = x - row * d.pitch;
-      uint32_t w = 0;
-      while (col >= d.off[w + 1]) ++w;
-      for (;;) {
-        const uint4 val = *reinterpret_cast<const uint4*>(sm + 16ull * v);
-        const uint64_t seg = (uint64_t)(d.off[w + 1] - d.off[w]);
-        __stcs(reinterpret_cast<uint4*>(d.dst[w] + row * seg + (col - d.off[w])), val);
-        v += 32;
-        if (v >= v1) break;
-        col += 512;
-        while (col >= d.pitch) {
-          col -= d.pitch;
-          ++row;
-          w = 0;
-        }
-        while (col >= d.off[w + 1]) ++w;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
-  }
-}
-
 // ---------------------------------------------------------------- host side
 static const uint32_t kSize[13] = {1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8};
 
@@ -1448,91 +1329,6 @@ static size_t tile_smem(int kind) {
   return kind == K_COPY1 ? (size_t)kTileStages * kTileBox : (size_t)2 * kTileCastStages * kTileBox;
 }
 
-// ---- TMA row split (host): a run of descriptors that is all W column shards of one tensor
-// Opt-in ($HL_GATHER_SPLIT=1): measured slower than the interleaved tiles on one
-// B200 (profiles/r02_split.txt: 7B TP=8 column shards 0.59 vs 0.80 of HBM peak,
-// 70B 0.84 vs 0.98) — one thread issuing a bulk store per (row, shard) piece
-// is bound by the TMA unit's operation rate when pieces are 1-7 KiB.
-// Opt-in ($HL_GATHER_SPLIT=1). Measured against the interleaved tiles on one B200
-// (profiles/r02_split*.txt): 7B TP=8 column shards 0.84 vs 0.80 of HBM peak (it
-// wins on the 2,752-byte down_proj rows the 2 KiB tile boxes cut raggedly, loses
-// on the 1 KiB o_proj rows), 70B 0.89 vs 0.98 — no width rule wins on both, so the
-// tiles stay the default. $HL_SPLIT_MAX_SEG caps the shard width it takes.
-static bool splits_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("HL_GATHER_SPLIT");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-static uint64_t split_max_seg() {
-  static const uint64_t v = [] {
-    const char* e = getenv("HL_SPLIT_MAX_SEG");
-    return e ? strtoull(e, nullptr, 10) : ~0ull;
-  }();
-  return v;
-}
-
-// descs[i..i+W) is a full-row split when they are raw copies of equal row
-// counts at one pitch whose source ranges follow each other and add up to the
-// pitch (so the run reads every source byte exactly once), all 16-byte aligned.
-// Returns W (0 = not a split) and fills `d` (all but unit_begin) and its units.
-static uint32_t make_split(const hl_desc* descs, uint32_t i, uint32_t n, SplitDesc& d, uint64_t& units) {
-  const hl_desc& h = descs[i];
-  if (h.src_dtype != h.dst_dtype || h.src_dtype >= 13 || h.rows < 2) return 0;
-  const uint64_t es = kSize[h.src_dtype], pitch = h.src_pitch;
-  if (!h.src || pitch % 16 || h.src % 16 || pitch >= (1ull << 32)) return 0;
-  uint64_t cum = 0;
-  uint32_t w = 0;
-  for (uint32_t j = i; j < n && w < (uint32_t)kSplitMax; ++j, ++w) {
-    const hl_desc& g = descs[j];
-    const uint64_t width = g.row_elems * es;
-    if (g.src_dtype != h.src_dtype || g.dst_dtype != h.dst_dtype || g.rows != h.rows || g.src_pitch != pitch ||
-        g.src != h.src + cum || !g.dst || g.dst % 16 || width == 0 || width % 16 || cum + width > pitch ||
-        width > split_max_seg())
-      return 0;
-    d.dst[w] = g.dst;
-    d.off[w] = (uint32_t)cum;
-    cum += width;
-    if (cum == pitch) {
-      if (w == 0) return 0;  // one "shard" covering the row: a plain copy
-      d.off[w + 1] = (uint32_t)cum;
-      d.nw = w + 1;
-      d.src = h.src;
-      d.pitch = pitch;
-      d.total = h.rows * pitch;
-      units = (d.total + kBulkChunk - 1) / kBulkChunk;
-      return w + 1;
-    }
-  }
-  return 0;
-}
-
-static int launch_splits(SplitParams& p, cudaStream_t stream) {
-  if (p.total_units == 0) return HL_OK;
-  static std::mutex mu;
-  static bool attr[64] = {};
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (!attr[dev & 63]) {
-      cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem);
-      attr[dev & 63] = true;
-    }
-  }
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<uint64_t>(p.total_units, (uint64_t)sms * kSplitCtas);
-  split_kernel<<<grid, kSplitThreads, kSplitSmem, stream>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_error(HL_ECUDA, "split launch failed: %s", cudaGetErrorString(e));
-  g_launches.fetch_add(1);
-  p.n = 0;
-  p.total_units = 0;
-  return HL_OK;
-}
-
 static int launch_tiles(int kind, TileParams& p, cudaStream_t stream) {
   if (p.total_units == 0) return HL_OK;
   static std::mutex mu;
@@ -1617,11 +1413,6 @@ extern "C" int hl_gather_prepare(int device) {
     cudaFuncGetAttributes(&a, tile_kernel_of(kind));
     cudaFuncSetAttribute(tile_kernel_of(kind), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem(kind));
   }
-  {
-    cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, split_kernel);
-    cudaFuncSetAttribute(split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem);
-  }
   encode_tiled();
   cudaGetLastError();
   cudaSetDevice(prev);
@@ -1652,30 +1443,7 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
     tile_units[k].clear();
   }
   const bool use_tiles = tma && tiles_enabled();
-  // runs of descriptors that are all W column shards of one tensor: the row split kernel
-  static thread_local std::vector<SplitDesc> splits;
-  static thread_local std::vector<uint64_t> split_units;
-  static thread_local std::vector<uint8_t> in_split;
-  splits.clear();
-  split_units.clear();
-  in_split.assign(n, 0);
-  if (tma && splits_enabled()) {
-    for (uint32_t i = 0; i < n;) {
-      SplitDesc sd;
-      uint64_t su = 0;
-      const uint32_t w = make_split(descs, i, n, sd, su);
-      if (!w) {
-        ++i;
-        continue;
-      }
-      splits.push_back(sd);
-      split_units.push_back(su);
-      for (uint32_t j = i; j < i + w; ++j) in_split[j] = 1;
-      i += w;
-    }
-  }
   for (uint32_t i = 0; i < n; ++i) {
-    if (in_split[i]) continue;
     if (use_tiles) {
       const int kind = conversion_kind(descs[i].src_dtype, descs[i].dst_dtype);
       TileDesc t;
@@ -1745,23 +1513,6 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
       i = j;
     }
     int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
-    if (rc) return rc;
-  }
-  if (!splits.empty()) {
-    static thread_local SplitParams* sp = nullptr;  // ~30 KB
-    if (!sp) sp = new SplitParams();
-    sp->n = 0;
-    sp->total_units = 0;
-    for (size_t i = 0; i < splits.size(); ++i) {
-      splits[i].unit_begin = sp->total_units;
-      sp->d[sp->n++] = splits[i];
-      sp->total_units += split_units[i];
-      if (sp->n == (uint32_t)kMaxSplits) {
-        int rc = launch_splits(*sp, (cudaStream_t)stream);
-        if (rc) return rc;
-      }
-    }
-    int rc = launch_splits(*sp, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return HL_OK;

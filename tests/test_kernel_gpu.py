@@ -366,9 +366,8 @@ def test_interleaved_shard_groups_across_launches(world):
 def test_row_split_owner_pack(rows, cols, dt, world, lead):
     """All W column shards of one tensor in a row (the NCCL plane's owner pack),
     between unrelated descriptors: bit-exact against the oracle with sentinels
-    around every output. On the default path they run on the interleaved tile
-    kernels; tools/gpu_runs/r02_split.sh runs this test with HL_GATHER_SPLIT=1
-    (the opt-in row split kernel)."""
+    around every output (interleaved tile groups; uneven widths on the row
+    kernel)."""
     rng = np.random.default_rng(rows * 7 + cols + world)
     es = SIZES[dt]
     src = rng.integers(0, 256, size=lead + rows * cols * es + 4096 + 64, dtype=np.uint8)
