@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagedStages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(kConsumerWarps));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(32 * kConsumerWarps));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -843,10 +843,10 @@ __global__ void __launch_bounds__(kStagedThreads) staged_kernel(const __grid_con
         stg16(x.dst + (size_t)v * 16, convert_vec<K>(sp[i]));
       }
     }
-    // generic-proxy smem writes must be visible to the async proxy (the bulk store)
+    // generic-proxy smem writes must be visible to the async proxy (the bulk store); every
+    // consumer thread releases its own reads and writes of the stage on the empty barrier
     if constexpr (TS) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
   }
 }
 
