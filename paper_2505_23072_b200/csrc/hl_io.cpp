@@ -2,7 +2,8 @@
 // reference's execute_plan / transfer_from_file, ref transfer.py:305-389 and
 // device.py:238-288).
 //
-// Data path per chunk (default chunk 16 MiB, 4 KiB aligned):
+// Data path per chunk (the caller's slot size, 4 MiB from the loader; 2 MiB
+// chunks for plans under 2 GiB, 1 MiB for cold plans; 4 KiB aligned):
 //
 //   storage --pread (O_DIRECT, or buffered when the file is page-cache
 //   resident)--> pinned slot (worker-private ring, NUMA-local) --cudaMemcpyAsync
@@ -21,8 +22,10 @@
 // The ring is one pinned region per context (huge-page backed, first-touched
 // on the GPU's NUMA node, see ensure_ring_memory), allocated before the first
 // plan's workers start and reused by every later plan; its cost is reported in
-// hl_plan_stats.ring_setup_seconds. A plan that is mostly cold (O_DIRECT) runs
-// on a larger team (cold_workers) whose extra slots get a second region.
+// hl_plan_stats.ring_setup_seconds. A plan that is mostly cold (O_DIRECT) is
+// read by io_uring threads keeping many O_DIRECT reads in flight over the
+// team's slots (uring_loop), or, without io_uring, by a larger team of
+// blocking readers (cold_workers) whose extra slots get a second region.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdlib.h>
