@@ -708,13 +708,14 @@ def main():
         return fb
 
     kernels.TIMING = []
+    _native.gather_timing(True)  # CUDA events on the launch stream around each call's kernel launches
     vals, dom_ms, dom_bytes, k_ms, k_bytes, k_n = [], [], 0, 0.0, 0, 0
     launches_value = 0
     for i in range(args.warmup + args.steps):
         fb = fresh_fb()
         barrier()
         torch.cuda.synchronize()
-        kernels.TIMING.clear()
+        kernels.timings()  # drop anything recorded outside the step
         l0 = _native.kernel_launches()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -722,15 +723,16 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = max_over_ranks(e0.elapsed_time(e1))
+        timed = kernels.timings()  # [(ms, algorithmic bytes)] of this step's hl_gather calls
         if i >= args.warmup:
             vals.append(ms)
             launches_value += _native.kernel_launches() - l0
-            k_ms = sum(a.elapsed_time(b) for a, b, _ in kernels.TIMING)
-            k_bytes = sum(nb for _, _, nb in kernels.TIMING)
-            k_n = len(kernels.TIMING)
+            k_ms = sum(t for t, _ in timed)
+            k_bytes = sum(nb for _, nb in timed)
+            k_n = len(timed)
             # the dominant launch of the step (get_tensors issues a small head group first)
-            a_, b_, nb_ = max(kernels.TIMING, key=lambda t: t[2])
-            dom_ms.append(a_.elapsed_time(b_))
+            t_, nb_ = max(timed, key=lambda t: t[1])
+            dom_ms.append(t_)
             dom_bytes = nb_
         del outs
         torch.cuda.synchronize()
@@ -738,6 +740,7 @@ def main():
         fb._hosted, fb._peer = {}, None  # landed buffers (and their mappings) are shared across steps
         fb.close()
     kernels.TIMING = None
+    _native.gather_timing(False)
     value_leg_ms = statistics.median(vals)
     hbm_peak, peak_source = hbm_peak_gbs()
     achieved = dom_bytes / (statistics.mean(dom_ms) / 1e3) / 1e9 if dom_ms else None

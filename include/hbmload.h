@@ -261,6 +261,14 @@ uint32_t hl_gather_max_batch(void);
 
 /* Number of kernel launches hl_gather issued by this process so far. */
 uint64_t hl_kernel_launches(void);
+/* Launch timing for measurements (bench.py roofline): while enabled, every
+ * hl_gather call records a CUDA event pair on its stream around its kernel
+ * launches (after the host-side descriptor translation). hl_gather_timings
+ * waits for the recorded pairs, writes their elapsed milliseconds in call
+ * order (up to cap; *n = how many were recorded) and forgets them.
+ * hl_gather_timing(0/1) switches it and drops pending pairs. */
+int hl_gather_timing(int enable);
+int hl_gather_timings(float* ms, uint32_t cap, uint32_t* n);
 
 /* Load every hl_gather kernel variant for `device` ahead of use (CUDA loads
  * kernels lazily): call once per process, e.g. on a side thread while the first

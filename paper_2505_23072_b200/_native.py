@@ -123,6 +123,8 @@ SIGNATURES = {
     "hl_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
     "hl_gather_max_batch": (C.c_uint32, []),
     "hl_kernel_launches": (C.c_uint64, []),
+    "hl_gather_timing": (C.c_int, [C.c_int]),
+    "hl_gather_timings": (C.c_int, [C.POINTER(C.c_float), C.c_uint32, C.POINTER(C.c_uint32)]),
     "hl_gather_prepare": (C.c_int, [C.c_int]),
 }
 
@@ -162,6 +164,22 @@ def conversion_supported(src_code: int, dst_code: int) -> bool:
 
 def kernel_launches() -> int:
     return int(load().hl_kernel_launches())
+
+
+def gather_timing(enable: bool) -> None:
+    """Switch hl_gather's launch timing (events around each call's kernel launches)."""
+    check(load().hl_gather_timing(1 if enable else 0))
+
+
+def gather_timings() -> list[float]:
+    """Milliseconds of every hl_gather call recorded since the last fetch, in call order
+    (waits for them to finish)."""
+    lib = load()
+    n = C.c_uint32()
+    cap = 4096
+    arr = (C.c_float * cap)()
+    check(lib.hl_gather_timings(arr, cap, C.byref(n)))
+    return [float(arr[i]) for i in range(min(n.value, cap))]
 
 
 _prepared: set[int] = set()

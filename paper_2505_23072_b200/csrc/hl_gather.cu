@@ -1068,6 +1068,47 @@ static int conversion_kind(uint32_t s, uint32_t d) {
 
 static std::atomic<uint64_t> g_launches{0};
 
+// Optional launch timing (hl_gather_timing): a CUDA event pair per hl_gather
+// call, recorded on its stream right before the first kernel launch and after
+// the last one — the host-side descriptor translation stays outside, so a
+// short launch is timed as the kernels, not as the host path in front of them.
+static std::mutex g_timing_mu;
+static bool g_timing_on = false;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timing_events;
+
+struct LaunchTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit LaunchTimer(cudaStream_t st) : s(st) {
+    {
+      std::lock_guard<std::mutex> g(g_timing_mu);
+      if (!g_timing_on) return;
+    }
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess ||
+        cudaEventRecord(a, s) != cudaSuccess) {
+      cudaGetLastError();
+      release();
+    }
+  }
+  void done() {
+    if (!a) return;
+    if (cudaEventRecord(b, s) != cudaSuccess) {
+      cudaGetLastError();
+      release();
+      return;
+    }
+    std::lock_guard<std::mutex> g(g_timing_mu);
+    g_timing_events.emplace_back(a, b);
+    a = b = nullptr;
+  }
+  void release() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    a = b = nullptr;
+  }
+  ~LaunchTimer() { release(); }
+};
+
 // which: 0 = generic, 1 + RowClass = row kernel of that class
 template <class P, int K>
 static auto kernel_for(int which) -> void (*)(P) {
@@ -1390,6 +1431,38 @@ extern "C" uint32_t hl_gather_max_batch(void) { return kMaxDescs; }
 
 extern "C" uint64_t hl_kernel_launches(void) { return g_launches.load(); }
 
+extern "C" int hl_gather_timing(int enable) {
+  clear_error();
+  std::lock_guard<std::mutex> g(g_timing_mu);
+  g_timing_on = enable != 0;
+  for (auto& e : g_timing_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  g_timing_events.clear();
+  return HL_OK;
+}
+
+extern "C" int hl_gather_timings(float* ms, uint32_t cap, uint32_t* n) {
+  clear_error();
+  if (!n) return set_error(HL_EINVAL, "null argument");
+  std::lock_guard<std::mutex> g(g_timing_mu);
+  *n = (uint32_t)g_timing_events.size();
+  int rc = HL_OK;
+  for (size_t i = 0; i < g_timing_events.size(); ++i) {
+    auto& e = g_timing_events[i];
+    float t = -1.0f;
+    if (cudaEventSynchronize(e.second) != cudaSuccess || cudaEventElapsedTime(&t, e.first, e.second) != cudaSuccess) {
+      rc = set_error(HL_ECUDA, "launch timing: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    if (ms && i < cap) ms[i] = t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  g_timing_events.clear();
+  return rc;
+}
+
 extern "C" int hl_gather_prepare(int device) {
   // Load every kernel variant and set its launch attributes ahead of the first
   // hl_gather (CUDA loads kernels lazily, on first use): the loader calls this
@@ -1464,6 +1537,7 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
       present |= 1u << b;
     }
   }
+  LaunchTimer timer((cudaStream_t)stream);  // hl_gather_timing: events around the launches only
   static thread_local Params* p = nullptr;  // ~32 KB: keep it off the stack
   if (!p) p = new Params();
   // one launch per (conversion kind, kernel variant) present in the batch
@@ -1515,5 +1589,6 @@ extern "C" int hl_gather_ex(const hl_desc* descs, uint32_t n, void* stream, uint
     int rc = launch_tiles(kind, *tp, (cudaStream_t)stream);
     if (rc) return rc;
   }
+  timer.done();
   return HL_OK;
 }

@@ -55,9 +55,23 @@ def current_stream_ptr(device: torch.device) -> int:
 # issues the NVLink reads; untested on NVLink here: every gpurun box has one GPU).
 PEER_TMA = os.environ.get("HL_PEER_TMA") == "1"
 
-# Optional launch timing (bench.py): when a list, every run() appends
-# (start_event, end_event, algorithmic_bytes) recorded on the launch stream.
+# Optional launch timing (bench.py): when a list, every run() appends its
+# algorithmic bytes, and hl_gather records a CUDA event pair on the launch
+# stream around that call's kernel launches (after the host-side descriptor
+# translation); timings() pairs them up once the work is done.
 TIMING: list | None = None
+
+
+def timings() -> list[tuple[float, int]]:
+    """(milliseconds, algorithmic bytes) of every run() since TIMING was
+    (re)started, in order; clears both. Waits for the launches to finish."""
+    ms = _native.gather_timings()
+    nb = list(TIMING or [])
+    if TIMING is not None:
+        TIMING.clear()
+    if len(ms) != len(nb):
+        raise RuntimeError(f"launch timing: {len(ms)} event pairs for {len(nb)} runs")
+    return list(zip(ms, nb))
 
 _SIZE = [1, 1, 1, 2, 2, 4, 4, 8, 8, 2, 2, 4, 8]
 
@@ -89,11 +103,5 @@ def run(descs: list[Desc], device: torch.device, peer: bool = False, stream_ptr:
     if TIMING is None:
         _native.gather(descs, _raw_stream(device.index) if stream_ptr is None else stream_ptr, flags)
         return
-    stream = torch.cuda.current_stream(device) if stream_ptr is None else \
-        torch.cuda.ExternalStream(stream_ptr, device=device)
-    table, n = _native.pack(descs)  # host-side table build stays outside the timed launch
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    _native.launch(table, n, stream.cuda_stream, flags)
-    e1.record(stream)
-    TIMING.append((e0, e1, algorithmic_bytes(descs)))
+    _native.gather(descs, _raw_stream(device.index) if stream_ptr is None else stream_ptr, flags)
+    TIMING.append(algorithmic_bytes(descs))

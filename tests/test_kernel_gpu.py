@@ -382,3 +382,25 @@ def test_row_split_owner_pack(rows, cols, dt, world, lead):
     got, exp = run_both(src, cd, descs)
     assert _native.kernel_launches() > l0
     assert_same(got, exp)
+
+
+def test_launch_timing_pairs_every_call():
+    """hl_gather_timing / hl_gather_timings (bench.py's roofline timer): one
+    event pair per hl_gather call while enabled, positive durations in call
+    order, nothing recorded while disabled."""
+    dev = torch.device("cuda", 0)
+    src = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+    dst = torch.empty_like(src)
+    d = kernels.copy_desc(src.data_ptr(), dst.data_ptr(), src.numel(), DType.U8)
+    _native.gather_timing(False)
+    kernels.run([d], dev)
+    assert _native.gather_timings() == []
+    _native.gather_timing(True)
+    try:
+        for _ in range(3):
+            kernels.run([d], dev)
+        ms = _native.gather_timings()
+        assert len(ms) == 3 and all(t > 0 for t in ms), ms
+        assert _native.gather_timings() == []  # fetched pairs are forgotten
+    finally:
+        _native.gather_timing(False)
