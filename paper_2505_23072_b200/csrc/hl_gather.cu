@@ -1073,17 +1073,14 @@ static std::atomic<uint64_t> g_launches{0};
 // the last one — the host-side descriptor translation stays outside, so a
 // short launch is timed as the kernels, not as the host path in front of them.
 static std::mutex g_timing_mu;
-static bool g_timing_on = false;
+static std::atomic<bool> g_timing_on{false};
 static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timing_events;
 
 struct LaunchTimer {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s;
   explicit LaunchTimer(cudaStream_t st) : s(st) {
-    {
-      std::lock_guard<std::mutex> g(g_timing_mu);
-      if (!g_timing_on) return;
-    }
+    if (!g_timing_on.load(std::memory_order_relaxed)) return;  // the hot path: one relaxed load
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess ||
         cudaEventRecord(a, s) != cudaSuccess) {
       cudaGetLastError();
