@@ -42,14 +42,20 @@ for it in range(4):
     ld = SafeTensorsFileLoader(SingleGroup(), "host", config=LoaderConfig(auto_release=True))
     ld.add_filenames({0: paths})
     fb = ld.copy_files_to_device()
+    t1 = time.perf_counter()
     outs = [fb.get_tensor(k) for k in keys]
+    t2 = time.perf_counter()
     tail = outs[-1].torch.reshape(-1)[:32].view(torch.uint8).cpu()
     torch.cuda.synchronize()
     s = time.perf_counter() - t
     st = ld.last_transfer_stats
+    ms = torch.cuda.memory_stats()
     row = {"iter": it, "seconds_to_ready": round(s, 3), "GBps": round(tensor_bytes / s / 1e9, 2),
+           "copy_s": round(t1 - t, 3), "retrieve_s": round(t2 - t1, 3), "drain_s": round(s - (t2 - t), 3),
            "engine_s": round(st.engine_seconds, 3), "io_modes": st.io_modes, "io_threads": st.io_threads,
-           "peak_hbm_GB": round(torch.cuda.max_memory_allocated() / 1e9, 1)}
+           "peak_allocated_GB": round(ms.get("allocated_bytes.all.peak", 0) / 1e9, 1),
+           "peak_reserved_GB": round(ms.get("reserved_bytes.all.peak", 0) / 1e9, 1),
+           "alloc_retries": ms.get("num_alloc_retries"), "cuda_malloc_retries": ms.get("num_device_alloc")}
     if it == 3:  # bit-exact against the file bytes, 24 sampled tensors (the largest included)
         rng = random.Random(7)
         sample = rng.sample(keys, 23) + [max(keys, key=lambda k: where[k][2])]
