@@ -70,6 +70,7 @@ DEFAULT_ALIGN_BOUNCE = 16 * 1024 * 1024  # kept for API parity; the realign kern
 CARVE_CHUNK = 1 << 30                # largest shared chunk per-key outputs are carved from
 CARVE_SMALL = 1 << 20                # outputs below this (norms, biases) share their own chunks...
 CARVE_SMALL_CHUNK = 16 << 20         # ...of this size, so keeping one of them pins 16 MiB, not 1 GiB
+CARVE_OPEN = 16                      # chunks with room left that a new output may be carved from
 
 
 class BackendKind(Enum):
@@ -217,8 +218,7 @@ class DevicePool:
         self.pooled_bytes = 0
         self.cumulative_pooled_bytes = 0
         # carving: per-key outputs sliced from shared chunks (see _carve)
-        self._chunk: torch.Tensor | None = None
-        self._chunk_off = 0
+        self._open: list[list] = []  # [chunk tensor, next free offset]: chunks with room left (first fit)
         self._small: torch.Tensor | None = None  # chunk for outputs under CARVE_SMALL
         self._small_off = 0
         self._expect = 0
@@ -232,7 +232,7 @@ class DevicePool:
     def end_carving(self) -> None:
         """Drop the pool's reference to the current chunk (slices keep theirs)."""
         with self._lock:
-            self._chunk, self._chunk_off, self._expect = None, 0, 0
+            self._open, self._expect = [], 0
             self._small, self._small_off = None, 0
 
     def _carve(self, nbytes: int) -> torch.Tensor:
@@ -256,13 +256,21 @@ class DevicePool:
             t = self._small[self._small_off:self._small_off + nbytes]
             self._small_off += (nbytes + 255) & ~255
             return t
-        if self._chunk is None or self._chunk_off + nbytes > self._chunk.numel():
+        # first fit over the chunks that still have room: big weights (a 70B MLP matrix is
+        # 470 MB of a 1 GiB chunk) leave gaps that later, smaller outputs fill; carving only
+        # from the newest chunk wasted 25-33% of HBM on 70B (profiles/r02_carve_fit.txt)
+        for ent in self._open:
+            if ent[1] + nbytes <= ent[0].numel():
+                break
+        else:
             size = max(nbytes, min(CARVE_CHUNK, max(self._expect, nbytes)))
-            self._chunk = torch.empty(size, dtype=torch.uint8, device=self.device)
-            self._chunk_off = 0
-        t = self._chunk[self._chunk_off:self._chunk_off + nbytes]
-        self._chunk_off += (nbytes + 255) & ~255
+            ent = [torch.empty(size, dtype=torch.uint8, device=self.device), 0]
+            self._open.append(ent)
+        t = ent[0][ent[1]:ent[1] + nbytes]
+        ent[1] += (nbytes + 255) & ~255
         self._expect = max(0, self._expect - nbytes)
+        # chunks with less than a small output's room left are closed (the list stays short)
+        self._open = [e for e in self._open if e[0].numel() - e[1] >= CARVE_SMALL][-CARVE_OPEN:]
         return t
 
     def allocate(self, size: int, zero: bool = False, carve: bool = False) -> DeviceBuffer:
@@ -288,7 +296,7 @@ class DevicePool:
                     try:
                         t = self._carve(max(size, 1) + 16)
                     except torch.OutOfMemoryError:
-                        self._chunk, self._chunk_off = None, 0
+                        self._open = []
                         self._small, self._small_off = None, 0
                         t = torch.empty(max(size, 1) + 16, dtype=torch.uint8, device=self.device)
                 else:
