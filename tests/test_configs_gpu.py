@@ -53,6 +53,18 @@ def _free_disk_after_module():
 def _gen(name, arch, header="aligned", layers=None, max_bytes=None):
     d = DATA / name
     if not (d / "READY").exists():
+        import shutil
+
+        need = int(sum(synth.nbytes(e) for e in synth.entries(arch, layers)) * 1.02) + (1 << 30)
+        DATA.mkdir(parents=True, exist_ok=True)
+        for other in sorted(DATA.iterdir()):  # this module's earlier corpora go first
+            if shutil.disk_usage(DATA).free >= need:
+                break
+            if other != d:
+                shutil.rmtree(other, ignore_errors=True)
+        if shutil.disk_usage(DATA).free < need:
+            pytest.skip(f"{name}: needs {need / 1e9:.1f} GB of free disk under {DATA}, "
+                        f"{shutil.disk_usage(DATA).free / 1e9:.1f} GB left")
         synth.generate(arch, d, header=header, device="cuda", layers=layers, max_bytes=max_bytes)
         (d / "READY").write_text("ok")
     return sorted(d.glob("*.safetensors"))
