@@ -7,11 +7,17 @@
  * reference) keeps the reference's semantics and calls these entry points for
  * everything that touches bytes:
  *
- *   bulk file -> HBM I/O         hl_ctx_create / hl_execute_plan / hl_transfer_from_file
+ *   bulk file -> HBM I/O         hl_ctx_create / hl_execute_plan(_after/_async) /
+ *                                hl_transfer_from_file (pinned ring + per-worker H2D streams;
+ *                                cold plans on io_uring O_DIRECT reads)
  *   realign / shard / cast       hl_gather (one batched sm_100a entry point, descriptor table;
  *                                TMA bulk-copy / TMA-staged kernels for contiguous tensors,
- *                                LDG/STG warp kernels for column shards)
+ *                                2-D tensor-map TMA tiles for column shards, LDG/STG warp
+ *                                kernels for the rest and for peer pulls)
+ *   peer memory                  hl_ipc_export / hl_ipc_import / hl_enable_peer_access
+ *   placement                    hl_topology_resolve / hl_ctx_cpus / hl_storage_numa_node
  *   page-cache control           hl_file_residency / hl_drop_cache
+ *   measurement                  hl_kernel_launches / hl_gather_timing(s)
  *
  * Conventions
  *   - Plain C types only: pointers, sizes, integers. No torch types. Device
