@@ -148,3 +148,42 @@ def test_reference_outcomes_on_fuzzed_headers():
         if got != c["expect"]:
             mismatches.append((c["tag"], c["expect"], got))
     assert not mismatches, mismatches[:5]
+
+
+def test_entry_fast_path_matches_the_full_checker():
+    """format._entry_fast (the well-formed-header shortcut) returns what
+    format._entry returns and raises what it raises, over random entries:
+    valid ones and every kind of malformed field (wrong types, bools as
+    ints, negative dims/offsets, unknown dtypes, missing or extra keys)."""
+    import random
+
+    from paper_2505_23072_b200 import format as F
+
+    rng = random.Random(5)
+    tags = [d.value for d in F.DType] + ["F8", "bf16", 3, None]
+
+    def val(kind):
+        return rng.choice({
+            "int": [0, 1, 7, 4096, -1, True, False, 2.0, "3", None],
+            "list": [[], [1, 2], [0], [3, -1], [True, 2], [1.0], "12", None, [1, [2]]],
+        }[kind])
+
+    for _ in range(4000):
+        e = {}
+        if rng.random() < 0.95:
+            e["dtype"] = rng.choice(tags)
+        if rng.random() < 0.95:
+            e["shape"] = val("list") if rng.random() < 0.3 else [rng.randint(0, 9) for _ in range(rng.randint(0, 3))]
+        if rng.random() < 0.95:
+            e["data_offsets"] = val("list") if rng.random() < 0.3 else [rng.randint(0, 99), rng.randint(0, 99)]
+        if rng.random() < 0.1:
+            e["extra"] = 1
+        obj = e if rng.random() < 0.97 else rng.choice([[1], "x", 3])
+
+        def run(fn):
+            try:
+                return ("ok", fn("t", obj))
+            except Exception as ex:  # noqa: BLE001 - compared by class and message
+                return ("err", type(ex).__name__, str(ex))
+
+        assert run(F._entry_fast) == run(F._entry), obj
